@@ -1,0 +1,610 @@
+"""Per-iteration engine: schedule -> KV apply -> launch -> stage execution -> commit.
+
+Drop-in for `pkg/src/tokensim/engine.py` (same constructor, `step`, `run`,
+`raw_data`, public `in_flight`, `kv`, `clock`; same `RawRunData`). Two
+things differ by design:
+
+1. **O(active) scheduling.** The reference rescans every request for #WP
+   and #RD and re-sorts both queues at every schedule point
+   (`engine.py:399-400, 411-419`; 12.7 s of 17.0 s at 2k requests, SURVEY
+   §0.6). Here #WP/#RD are counters updated at the five transitions that
+   change them (arrival, launch, commit, finish, preempt) and the queues
+   are kept FCFS-sorted by insertion, so a schedule step touches only the
+   requests it plans.
+2. **Real execution.** An optional `executor` receives each launched
+   micro-batch with its device metadata (block-table deltas, per-sequence
+   row/start/length, which rows emit a token) and runs it on the GPU stages;
+   `_commit` retires it. `Engine` keeps the reference's virtual clock
+   (cost model) so its decisions are bit-exact with the reference while the
+   GPU does the real work; `ServingEngine` (serving.py) drives the same state
+   machine from measured time instead.
+
+Semantics preserved (each cited at its use below): events at
+one timestamp drain in push order, then exactly one schedule attempt; #RD
+counts in-flight decodes; #WP subtracts in-flight chunks; LIFO victims drawn
+from the decode-ready queue including this plan's decodes; self-preemption;
+decode context recomputed after allocation; commit decodes before chunks.
+"""
+
+from __future__ import annotations
+
+import heapq
+from bisect import bisect_left, insort
+from dataclasses import dataclass, field
+
+from .errors import ConfigError, UnschedulableError
+from .kvcache import KvCacheState, KvConfig, PagedKvCache, pages_needed
+from .metrics import IterationRecord, RequestRecord
+from .sched import MicroBatchPlan, ThrottleConfig, fill_prefill, prefill_token_limit, throttle_decode
+from .workload import RequestSpec
+
+SCHEDULERS = ("throttle", "sarathi")
+
+ARRIVAL = "arrival"
+SCHEDULE_POINT = "schedule_point"
+STAGE_COMPLETE = "stage_complete"
+TRANSFER_COMPLETE = "transfer_complete"
+_EV_ARRIVAL, _EV_STAGE, _EV_XFER = 0, 1, 2
+
+
+@dataclass(frozen=True)
+class StageCostModel:
+    """Virtual-clock stage latency: c0 + c_tok*tokens + c_ctx*decode_ctx/1024 (`engine.py:45-57`)."""
+
+    c0: float = 1.0
+    c_tok: float = 0.01
+    c_ctx: float = 0.1
+
+    def __post_init__(self) -> None:
+        if min(self.c0, self.c_tok, self.c_ctx) < 0:
+            raise ConfigError("stage cost coefficients must be >= 0")
+        if self.c0 + self.c_tok <= 0:
+            raise ConfigError("need c0 + c_tok > 0 so nonempty batches take time")
+
+
+@dataclass(frozen=True)
+class CommModel:
+    """Virtual-clock activation hand-off: latency + tokens*bytes/bandwidth (`engine.py:60-82`)."""
+
+    latency_ms: float = 0.1
+    bytes_per_token: float = 16384.0
+    bandwidth_bytes_per_ms: float = 20.79e6
+
+    def __post_init__(self) -> None:
+        if self.bandwidth_bytes_per_ms <= 0:
+            raise ConfigError(f"bandwidth must be > 0, got {self.bandwidth_bytes_per_ms}")
+        if self.latency_ms < 0 or self.bytes_per_token < 0:
+            raise ConfigError("comm latency and payload must be >= 0")
+
+    @classmethod
+    def pcie(cls, latency_ms: float = 0.1, bytes_per_token: float = 16384.0) -> "CommModel":
+        return cls(latency_ms, bytes_per_token, 20.79e6)
+
+    @classmethod
+    def network(cls, latency_ms: float = 0.1, bytes_per_token: float = 16384.0) -> "CommModel":
+        return cls(latency_ms, bytes_per_token, 73.28e9 / 8.0 / 1000.0)
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    depth: int = 4
+    cost: StageCostModel = StageCostModel()
+    comm: CommModel = CommModel()
+
+    def __post_init__(self) -> None:
+        if self.depth < 1:
+            raise ConfigError(f"pipeline.depth must be >= 1, got {self.depth}")
+
+
+def stage_time(plan: MicroBatchPlan, cost: StageCostModel) -> float:
+    if plan.is_empty():
+        return 0.0
+    return cost.c0 + cost.c_tok * plan.total_tokens + cost.c_ctx * plan.decode_context_tokens / 1024.0
+
+
+def transfer_time(plan: MicroBatchPlan, comm: CommModel) -> float:
+    return comm.latency_ms + plan.total_tokens * comm.bytes_per_token / comm.bandwidth_bytes_per_ms
+
+
+def bubble_accounting(busy_intervals: list[list[tuple[float, float]]], makespan_ms: float) -> list[float]:
+    """Idle fraction of [0, makespan] per stage; intervals must be ordered and disjoint (`engine.py:108-125`)."""
+    out = []
+    for ivs in busy_intervals:
+        busy = 0.0
+        last = None
+        for a, b in ivs:
+            if b < a or (last is not None and a < last):
+                raise ValueError("stage busy intervals overlap or are out of order")
+            busy += b - a
+            last = b
+        out.append(0.0 if makespan_ms <= 0 else (makespan_ms - busy) / makespan_ms)
+    return out
+
+
+class _Req:
+    __slots__ = ("spec", "key", "target", "done", "inflight", "generated", "preemptions",
+                 "incarnation", "arrived", "decoding", "in_flight", "first_ms", "finish_ms", "row")
+
+    def __init__(self, spec: RequestSpec):
+        self.spec = spec
+        self.key = (spec.arrival_ms, spec.id)
+        self.target = spec.input_tokens
+        self.done = 0
+        self.inflight = 0
+        self.generated = 0
+        self.preemptions = 0
+        self.incarnation = 0
+        self.arrived = False
+        self.decoding = False
+        self.in_flight = False
+        self.first_ms = None
+        self.finish_ms = None
+        self.row = -1
+
+    @property
+    def finished(self) -> bool:
+        return self.finish_ms is not None
+
+
+@dataclass
+class SeqMeta:
+    """One sequence of a launched micro-batch, in plan order (decodes, then chunks)."""
+
+    request_id: int
+    row: int          # block-table / token-history row
+    start: int        # tokens already in the KV cache before this batch
+    n_new: int        # tokens this batch appends (1 for a decode)
+    emits: bool       # this batch samples the sequence's next token
+
+
+@dataclass
+class BatchMeta:
+    """Everything a stage worker needs for one micro-batch (the paper's pre-broadcast metadata)."""
+
+    seq: int
+    seqs: list[SeqMeta]
+    page_deltas: object                   # int32 [n, 3] (row, page_index, page_id)
+    new_prompts: list[tuple[int, int]] = field(default_factory=list)  # (request_id, row)
+
+    @property
+    def n_tokens(self) -> int:
+        return sum(s.n_new for s in self.seqs)
+
+
+@dataclass
+class _Batch:
+    seq: int
+    plan: MicroBatchPlan
+    stage_ms: float
+    transfer_ms: float
+    meta: BatchMeta | None = None
+
+
+@dataclass
+class RawRunData:
+    requests: list[RequestRecord]
+    iterations: list[IterationRecord]
+    busy_intervals: list[list[tuple[float, float]]]
+    stage_spans: list[tuple[int, int, float, float]]
+    makespan_ms: float
+    committed_tokens: int
+    discarded_tokens: int
+    preemptions: int
+    truncated: bool
+    events: list[dict] | None = None
+
+    def bubble_fractions(self) -> list[float]:
+        return bubble_accounting(self.busy_intervals, self.makespan_ms)
+
+
+class EngineCore:
+    """Request state machine shared by the virtual-clock and wall-clock drivers."""
+
+    def __init__(self, requests: list[RequestSpec], scheduler: str = "throttle",
+                 pipeline: PipelineConfig | None = None, kv_config: KvConfig | None = None,
+                 throttle: ThrottleConfig | None = None, token_budget: int = 2048,
+                 executor=None, max_rows: int | None = None):
+        if scheduler not in SCHEDULERS:
+            raise ConfigError(f"scheduler must be one of {SCHEDULERS}, got {scheduler!r}")
+        self._scheduler = scheduler
+        self._pipeline = pipeline if pipeline is not None else PipelineConfig()
+        kv_config = kv_config if kv_config is not None else KvConfig(total_pages=4096, page_size=16)
+        self._throttle = throttle if throttle is not None else ThrottleConfig()
+        if token_budget < 1:
+            raise ConfigError(f"token_budget must be >= 1, got {token_budget}")
+        self._token_budget = token_budget
+        ids: set[int] = set()
+        prev = None
+        for spec in requests:
+            if spec.id in ids:
+                raise ConfigError(f"duplicate request id {spec.id}")
+            ids.add(spec.id)
+            if prev is not None and spec.arrival_ms < prev:
+                raise ConfigError("workload must be sorted by arrival time")
+            prev = spec.arrival_ms
+            need = pages_needed(0, spec.input_tokens + spec.output_tokens - 1, kv_config.page_size)
+            if need > kv_config.total_pages:
+                raise UnschedulableError(
+                    f"request {spec.id} needs {need} KV pages over its lifetime "
+                    f"but the cache has only {kv_config.total_pages}", (spec.id,))
+        self._reqs: dict[int, _Req] = {s.id: _Req(s) for s in requests}
+        self._order = [s.id for s in requests]
+        self.executor = executor
+        self.kv: KvCacheState = PagedKvCache(kv_config) if executor is not None else KvCacheState(kv_config)
+        self._rows_free: list[int] = []
+        self._rows_next = 0
+        self._max_rows = max_rows if max_rows is not None else max(1, len(requests))
+        self.clock = 0.0
+        self.makespan_ms = 0.0
+        self.committed_tokens = 0
+        self.discarded_tokens = 0
+        self.preemptions = 0
+        self.truncated = False
+        depth = self._pipeline.depth
+        self.in_flight: dict[int, _Batch] = {}
+        self._waiting: list[tuple[float, int]] = []   # FCFS keys, kept sorted
+        self._ready: list[tuple[float, int]] = []     # decode-ready FCFS keys, kept sorted
+        self._wp = 0
+        self._rd = 0
+        self._free_at = [0.0] * depth
+        self._busy: list[list[tuple[float, float]]] = [[] for _ in range(depth)]
+        self._spans: list[tuple[int, int, float, float]] = []
+        self._iters: list[IterationRecord] = []
+        self._events: list[dict] | None = None
+        self._seq = 0
+        self._pending_prompts: list[tuple[int, int]] = []
+
+    # -- logging ---------------------------------------------------------------
+
+    def _log(self, t: float, kind: str, stage, batch, plan: MicroBatchPlan | None) -> None:
+        if self._events is not None:
+            self._events.append({"time_ms": t, "kind": kind, "stage": stage, "batch": batch,
+                                 "prefill_tokens": 0 if plan is None else plan.prefill_tokens,
+                                 "decode_tokens": 0 if plan is None else plan.decode_tokens})
+
+    # -- transitions that move #WP / #RD -------------------------------------------
+
+    def _arrive(self, rid: int) -> None:
+        r = self._reqs[rid]
+        r.arrived = True
+        self._wp += r.target - r.done - r.inflight
+        insort(self._waiting, r.key)
+
+    def _finish(self, r: _Req, t: float) -> None:
+        r.finish_ms = t
+        if r.decoding:
+            self._rd -= 1
+        r.decoding = False
+        self.kv.release(r.spec.id)
+        if r.row >= 0:
+            if isinstance(self.kv, PagedKvCache):
+                self.kv.unbind_row(r.spec.id)
+            if self.executor is not None:
+                self.executor.on_finish(r.spec.id, r.row)
+            self._rows_free.append(r.row)
+            r.row = -1
+
+    def _enter_decode(self, r: _Req) -> None:
+        r.decoding = True
+        self._rd += 1
+
+    def _preempt(self, rid: int) -> None:
+        """Evict and queue for recompute (`engine.py:371-384`)."""
+        r = self._reqs[rid]
+        self.kv.release(rid)
+        self.preemptions += 1
+        r.preemptions += 1
+        self.discarded_tokens += r.incarnation
+        r.incarnation = 0
+        # The rebuilt cache is the prompt plus every generated token but the newest.
+        r.target = r.spec.input_tokens + max(r.generated - 1, 0)
+        r.done = 0
+        if r.decoding:
+            self._rd -= 1
+        r.decoding = False
+        self._wp += r.target
+        _remove_key(self._ready, r.key)
+        insort(self._waiting, r.key)
+
+    def _commit(self, t: float, batch: _Batch) -> None:
+        """Last-stage commit (`engine.py:334-364`): decodes first, then prefill chunks."""
+        plan = batch.plan
+        del self.in_flight[batch.seq]
+        if self.executor is not None:
+            self.executor.retire(batch.seq)
+        self.committed_tokens += plan.total_tokens
+        for rid in plan.decode_ids:
+            r = self._reqs[rid]
+            r.in_flight = False
+            r.generated += 1
+            r.incarnation += 1
+            if r.generated >= r.spec.output_tokens:
+                self._finish(r, t)
+            else:
+                insort(self._ready, r.key)
+        for rid, n in plan.prefill_chunks:
+            r = self._reqs[rid]
+            r.in_flight = False
+            r.inflight = 0
+            r.done += n
+            r.incarnation += n
+            if r.done >= r.target:
+                self._enter_decode(r)
+                if r.generated == 0:
+                    r.generated = 1      # the final prompt chunk yields the first token
+                    r.first_ms = t
+                    if r.generated >= r.spec.output_tokens:
+                        self._finish(r, t)
+                        continue
+                insort(self._ready, r.key)
+            else:
+                insort(self._waiting, r.key)
+
+    # -- scheduling ----------------------------------------------------------------
+
+    def _plan(self) -> MicroBatchPlan:
+        """Snapshot + planner call; O(planned) thanks to the counters (`engine.py:410-445`)."""
+        kv = self.kv
+        ps = kv.config.page_size
+        free = kv.free_pages
+        reqs = self._reqs
+        if self._scheduler == "throttle":
+            n_dec = throttle_decode(self._rd, self._pipeline.depth)
+            chosen = [k[1] for k in self._ready[:n_dec]]
+            limit = prefill_token_limit(self._wp, free / kv.config.total_pages, self._throttle)
+        else:
+            chosen = [k[1] for k in self._ready]
+            limit = min(max(0, self._token_budget - len(chosen)), self._wp)
+        stored = [kv.stored_tokens(rid) for rid in chosen]
+        reserved = sum(1 for s in stored if s % ps == 0)
+
+        def cands():
+            for _, rid in self._waiting:
+                r = reqs[rid]
+                yield rid, r.target - r.done, kv.stored_tokens(rid)
+
+        chunks = fill_prefill(cands(), limit, free - reserved, ps)
+        return MicroBatchPlan(chosen, chunks, sum(stored) + len(stored))
+
+    def _bind_row(self, rid: int) -> None:
+        r = self._reqs[rid]
+        if r.row >= 0:
+            return
+        if self._rows_free:
+            r.row = self._rows_free.pop()
+        else:
+            if self._rows_next >= self._max_rows:
+                raise ConfigError(f"out of block-table rows (max_rows={self._max_rows})")
+            r.row = self._rows_next
+            self._rows_next += 1
+        self.kv.bind_row(rid, r.row)
+        self._pending_prompts.append((rid, r.row))
+
+    def _apply_kv(self, plan: MicroBatchPlan) -> bool:
+        """Allocate the plan's pages, evicting LIFO decodes on failure (`engine.py:447-480`)."""
+        kv = self.kv
+        paged = isinstance(kv, PagedKvCache)
+        mutated = False
+        kept: list[int] = []
+        dropped: set[int] = set()
+        for rid in plan.decode_ids:
+            if rid in dropped:
+                continue
+            ok = True
+            while not kv.allocate(rid, 1):
+                # Victims come from the decode-ready queue, which still holds this
+                # plan's decodes (`engine.py:460-461`); the latest arrival loses.
+                victim = self._ready[-1][1]
+                self._preempt(victim)
+                mutated = True
+                dropped.add(victim)
+                if victim == rid:
+                    ok = False
+                    break
+                if victim in kept:
+                    kept.remove(victim)
+            if ok:
+                kept.append(rid)
+        if len(kept) != len(plan.decode_ids):
+            plan.decode_ids = kept
+        plan.decode_context_tokens = sum(kv.stored_tokens(rid) for rid in kept)
+        for rid, n in plan.prefill_chunks:
+            if paged:
+                self._bind_row(rid)
+            if not kv.allocate(rid, n):
+                raise AssertionError("prefill pages were reserved at planning time")
+        return mutated
+
+    def _try_plan(self) -> MicroBatchPlan | None:
+        """Plan + allocate; re-plan after an eviction that emptied the plan (`engine.py:391-408`)."""
+        while True:
+            if not self._waiting and not self._ready:
+                return None
+            plan = self._plan()
+            mutated = self._apply_kv(plan)
+            if not plan.is_empty():
+                return plan
+            if not mutated:
+                return None
+
+    def _make_batch(self, t: float, plan: MicroBatchPlan) -> _Batch:
+        """Launch bookkeeping (`engine.py:482-516`) plus the device metadata."""
+        seq = self._seq
+        self._seq += 1
+        batch = _Batch(seq, plan, stage_time(plan, self._pipeline.cost),
+                       transfer_time(plan, self._pipeline.comm))
+        reqs = self._reqs
+        metas: list[SeqMeta] | None = [] if self.executor is not None else None
+        for rid in plan.decode_ids:
+            r = reqs[rid]
+            r.in_flight = True
+            if metas is not None:
+                # stored_tokens already counts the token being appended now.
+                metas.append(SeqMeta(rid, r.row, self.kv.stored_tokens(rid) - 1, 1, True))
+        for rid, n in plan.prefill_chunks:
+            r = reqs[rid]
+            r.in_flight = True
+            r.inflight = n
+            self._wp -= n
+            if metas is not None:
+                metas.append(SeqMeta(rid, r.row, r.done, n,
+                                     r.done + n >= r.target and r.generated == 0))
+        _remove_prefix_ids(self._ready, plan.decode_ids, reqs)
+        _remove_prefix_ids(self._waiting, [rid for rid, _ in plan.prefill_chunks], reqs)
+        if metas is not None:
+            batch.meta = BatchMeta(seq, metas, self.kv.take_deltas(), self._pending_prompts)
+            self._pending_prompts = []
+        self.in_flight[seq] = batch
+        self._iters.append(IterationRecord(seq, t, plan.prefill_tokens, plan.decode_tokens))
+        return batch
+
+    # -- results -------------------------------------------------------------------
+
+    def _records(self) -> list[RequestRecord]:
+        recs = [RequestRecord(r.spec.id, r.spec.arrival_ms, r.first_ms, r.finish_ms,
+                              r.spec.input_tokens, r.spec.output_tokens, r.preemptions)
+                for r in self._reqs.values()]
+        recs.sort(key=lambda x: x.id)
+        return recs
+
+    def raw_data(self) -> RawRunData:
+        if self.truncated:
+            lim = self.makespan_ms
+            self._busy = [[(a, min(b, lim)) for a, b in ivs if a < lim] for ivs in self._busy]
+            self._spans = [(q, s, a, min(b, lim)) for q, s, a, b in self._spans if a < lim]
+        return RawRunData(self._records(), list(self._iters), [list(v) for v in self._busy],
+                          list(self._spans), self.makespan_ms, self.committed_tokens,
+                          self.discarded_tokens, self.preemptions, self.truncated,
+                          None if self._events is None else list(self._events))
+
+
+def _remove_key(keys: list, key) -> None:
+    i = bisect_left(keys, key)
+    if i < len(keys) and keys[i] == key:
+        del keys[i]
+    else:  # pragma: no cover - state corruption
+        raise AssertionError(f"key {key} not queued")
+
+
+def _remove_prefix_ids(keys: list, ids: list[int], reqs: dict) -> None:
+    """Drop launched ids; they are almost always a prefix of the FCFS queue."""
+    if not ids:
+        return
+    n = len(ids)
+    if n <= len(keys) and all(keys[i][1] == ids[i] for i in range(n)):
+        del keys[:n]
+        return
+    for rid in ids:
+        _remove_key(keys, reqs[rid].key)
+
+
+class Engine(EngineCore):
+    """Virtual-clock engine: the reference's discrete-event timeline, optionally driving GPUs.
+
+    Time advances by `StageCostModel`/`CommModel`, so every decision is
+    bit-exact with `tokensim.Engine` on the same trace; with an executor each
+    launched micro-batch also runs on the device stages (launch at
+    `_launch`, retire at the last-stage commit).
+    """
+
+    def __init__(self, requests: list[RequestSpec], scheduler: str = "throttle",
+                 pipeline: PipelineConfig | None = None, kv_config: KvConfig | None = None,
+                 throttle: ThrottleConfig | None = None, token_budget: int = 2048,
+                 horizon_ms: float | None = None, record_events: bool = False,
+                 executor=None, max_rows: int | None = None):
+        super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget,
+                         executor, max_rows)
+        if horizon_ms is not None and horizon_ms < 0:
+            raise ConfigError(f"horizon_ms must be >= 0, got {horizon_ms}")
+        self._horizon = horizon_ms
+        self._events = [] if record_events else None
+        depth = self._pipeline.depth
+        self._expect = [0] * depth
+        self._arrived_at: list[dict[int, float]] = [dict() for _ in range(depth)]
+        self._heap: list[tuple[float, int, int, int, int]] = []
+        self._eseq = 0
+        self._unfinished = len(self._reqs)
+        for rid in self._order:
+            self._push(self._reqs[rid].spec.arrival_ms, _EV_ARRIVAL, rid, 0)
+
+    def _push(self, t: float, kind: int, a: int, b: int) -> None:
+        heapq.heappush(self._heap, (t, self._eseq, kind, a, b))
+        self._eseq += 1
+
+    def step(self) -> bool:
+        """Drain every event at the next timestamp, then schedule at most once (`engine.py:265-289`)."""
+        heap = self._heap
+        if not heap:
+            stuck = tuple(sorted(rid for rid, r in self._reqs.items() if not r.finished))
+            if stuck:
+                raise UnschedulableError(f"no forward progress possible; stuck requests: {list(stuck)}", stuck)
+            return False
+        t = heap[0][0]
+        if self._horizon is not None and t > self._horizon:
+            self.truncated = True
+            self.makespan_ms = self._horizon
+            return False
+        self.clock = t
+        if t > self.makespan_ms:
+            self.makespan_ms = t
+        while heap and heap[0][0] == t:
+            _, _, kind, a, b = heapq.heappop(heap)
+            if kind == _EV_ARRIVAL:
+                self._arrive(a)
+                self._log(t, ARRIVAL, None, None, None)
+            elif kind == _EV_STAGE:
+                batch = self.in_flight[b]
+                self._log(t, STAGE_COMPLETE, a, b, batch.plan)
+                if a == self._pipeline.depth - 1:
+                    self._commit(t, batch)
+                else:
+                    self._push(t + batch.transfer_ms, _EV_XFER, a + 1, b)
+            else:
+                self._log(t, TRANSFER_COMPLETE, a, b, self.in_flight[b].plan)
+                self._arrived_at[a][b] = t
+                self._admit(a)
+        self._schedule(t)
+        return True
+
+    def run(self) -> RawRunData:
+        while self.step():
+            pass
+        return self.raw_data()
+
+    def _admit(self, stage: int) -> None:
+        """In-order stage entry: start = max(arrival, stage free) (`engine.py:317-330`)."""
+        pend = self._arrived_at[stage]
+        while self._expect[stage] in pend:
+            seq = self._expect[stage]
+            start = max(pend.pop(seq), self._free_at[stage])
+            end = start + self.in_flight[seq].stage_ms
+            self._busy[stage].append((start, end))
+            self._spans.append((seq, stage, start, end))
+            self._free_at[stage] = end
+            self._expect[stage] += 1
+            self._push(end, _EV_STAGE, stage, seq)
+
+    def _schedule(self, t: float) -> None:
+        if len(self.in_flight) >= self._pipeline.depth or self._free_at[0] > t:
+            return
+        plan = self._try_plan()
+        if plan is None:
+            return
+        batch = self._make_batch(t, plan)
+        self._log(t, SCHEDULE_POINT, 0, batch.seq, plan)
+        if self.executor is not None:
+            self.executor.launch(batch.meta)
+        end = t + batch.stage_ms
+        self._busy[0].append((t, end))
+        self._spans.append((batch.seq, 0, t, end))
+        self._free_at[0] = end
+        self._expect[0] += 1
+        self._push(end, _EV_STAGE, 0, batch.seq)
+
+
+def run(requests: list[RequestSpec], scheduler: str = "throttle", pipeline: PipelineConfig | None = None,
+        kv_config: KvConfig | None = None, throttle: ThrottleConfig | None = None,
+        token_budget: int = 2048, horizon_ms: float | None = None, record_events: bool = False,
+        executor=None) -> RawRunData:
+    return Engine(requests, scheduler, pipeline, kv_config, throttle, token_budget, horizon_ms,
+                  record_events, executor).run()

@@ -1,0 +1,125 @@
+"""Full engine timelines vs the reference (virtual clock, bit-exact).
+
+Fixtures from tests/golden/make_golden.py: C1 trace at depth 1/2/4, the
+reference's bursty fixture under its acceptance settings
+(`pkg/tests/test_acceptance.py:73-82, 170-229`), tick-simulator scenarios
+(`oracle_sim.py:397-469`) and the 100 conservation runs of criterion 8.
+"""
+import hashlib
+import json
+
+import pytest
+
+from golden_io import load
+from paper_2504_14775_b200 import (CommModel, Engine, KvConfig, PipelineConfig, RequestSpec, StageCostModel,
+                                    ThrottleConfig, UnschedulableError, build_report, run)
+from paper_2504_14775_b200.workload import ArrivalProcess, LengthDistribution, synthesize_requests
+
+ENGINE = load("engine_runs.json.gz")
+TRACES = load("traces.json.gz")
+TRACES.update(ENGINE["traces"])
+
+
+def _specs(rows):
+    return [RequestSpec(i, a, b, c) for i, (a, b, c) in enumerate(rows)]
+
+
+def _timeline(raw):
+    return {
+        "iterations": [[it.batch_seq, it.schedule_time_ms, it.prefill_tokens, it.decode_tokens] for it in raw.iterations],
+        "requests": [[r.id, r.arrival_ms, r.first_token_ms, r.completion_ms, r.preemption_count] for r in raw.requests],
+        "spans_sha": hashlib.sha256(json.dumps(raw.stage_spans).encode()).hexdigest(),
+        "busy_sha": hashlib.sha256(json.dumps(raw.busy_intervals).encode()).hexdigest(),
+        "makespan": raw.makespan_ms, "committed": raw.committed_tokens,
+        "discarded": raw.discarded_tokens, "preemptions": raw.preemptions, "truncated": raw.truncated,
+    }
+
+
+@pytest.mark.parametrize("case", ENGINE["runs"], ids=[r["name"] for r in ENGINE["runs"]])
+def test_engine_run_golden(case):
+    comm = CommModel.pcie() if case["comm"] == "pcie" else CommModel()
+    raw = run(_specs(TRACES[case["trace"]]), scheduler=case["scheduler"],
+              pipeline=PipelineConfig(depth=case["depth"], cost=StageCostModel(*case["cost"]), comm=comm),
+              kv_config=KvConfig(case["pages"], case["ps"]),
+              throttle=ThrottleConfig(T=case["T"], kv_thresh=case["thresh"]),
+              token_budget=case["budget"], horizon_ms=case["horizon"],
+              record_events="events_sha" in case)
+    got = _timeline(raw)
+    for k, v in got.items():
+        assert v == case[k], k
+    if "events_sha" in case:
+        assert hashlib.sha256(json.dumps(raw.events).encode()).hexdigest() == case["events_sha"]
+    if "report" in case:
+        rep = build_report(raw)
+        for k, v in case["report"].items():
+            assert getattr(rep, k) == v, k
+
+
+def test_acceptance_pins():
+    # The reference's pinned acceptance values (`test_acceptance.py:169-186`), recomputed here.
+    by = {r["name"]: r for r in ENGINE["runs"]}
+    assert by["bursty_throttle_p1024_T8_th0.05"]["report"]["token_stddev"] == pytest.approx(36.79826426303527, rel=1e-12)
+    assert by["bursty_sarathi_p1024_T8_th0.05"]["report"]["token_stddev"] == pytest.approx(113.29596236956067, rel=1e-12)
+    assert by["bursty_throttle_p192_T8_th0.0"]["preemptions"] == 142
+    assert by["bursty_throttle_p192_T8_th0.05"]["preemptions"] == 3
+
+
+SCEN = load("scenarios.json.gz")
+
+
+@pytest.mark.parametrize("i", range(len(SCEN)))
+def test_tick_scenarios(i):
+    s = SCEN[i]
+    reqs = [RequestSpec(a, b, c, d) for a, b, c, d in s["specs"]]
+    T, max_p, min_p, th, mode = s["throttle"]
+    eng = Engine(reqs, scheduler=s["scheduler"],
+                 pipeline=PipelineConfig(depth=s["depth"], cost=StageCostModel(float(s["c0"]), float(s["c_tok"]), float(s["c_ctx"])),
+                                         comm=CommModel(latency_ms=float(s["latency"]), bytes_per_token=0.0, bandwidth_bytes_per_ms=1.0)),
+                 kv_config=KvConfig(s["pages"], s["ps"]),
+                 throttle=ThrottleConfig(T=T, max_p=max_p, min_p=min_p, kv_thresh=th, mode=mode),
+                 token_budget=s["budget"])
+    stalled = []
+    try:
+        while eng.step():
+            pass
+    except UnschedulableError as exc:
+        stalled = sorted(exc.request_ids)
+    assert stalled == s["stalled"] == s["tick_stuck"]
+    raw = eng.raw_data()
+    assert [list(x) for x in raw.stage_spans] == s["spans"]
+    got = _timeline(raw)
+    for k in ("iterations", "requests", "committed", "discarded", "preemptions", "makespan"):
+        assert got[k] == s[k], k
+
+
+CONS = load("conservation.json.gz")
+
+
+@pytest.mark.parametrize("case", CONS, ids=[f"seed{c['seed']}" for c in CONS])
+def test_conservation_runs(case):
+    seed = case["seed"]
+    reqs = synthesize_requests(ArrivalProcess.poisson(40.0, seed),
+                               LengthDistribution.lognormal(60.0, 0.7, 15.0, 0.6, min_tokens=1, max_tokens=600), case["n"])
+    depth = case["depth"]
+    eng = Engine(reqs, scheduler=case["scheduler"], pipeline=PipelineConfig(depth=depth, comm=CommModel.pcie()),
+                 kv_config=KvConfig(case["pages"], 16), throttle=ThrottleConfig())
+    while eng.step():
+        # invariants of criterion 8 (`test_acceptance.py:288-300`)
+        assert len(eng.in_flight) <= depth
+        ids = [rid for b in eng.in_flight.values() for rid in b.plan.decode_ids + [r for r, _ in b.plan.prefill_chunks]]
+        assert len(ids) == len(set(ids))
+        assert eng.kv.free_pages + sum(eng.kv.pages(r) for r in eng.kv.holders) == eng.kv.config.total_pages
+    raw = eng.raw_data()
+    t = _timeline(raw)
+    assert hashlib.sha256(json.dumps(t["iterations"]).encode()).hexdigest() == case["iters_sha"]
+    assert hashlib.sha256(json.dumps(t["requests"]).encode()).hexdigest() == case["reqs_sha"]
+    assert t["spans_sha"] == case["spans_sha"]
+    assert (raw.preemptions, raw.committed_tokens, raw.discarded_tokens) == (case["preemptions"], case["committed"], case["discarded"])
+    lifetimes = sum(r.input_tokens + r.output_tokens - 1 for r in raw.requests)
+    assert raw.committed_tokens - raw.discarded_tokens == lifetimes
+
+
+def test_unschedulable_upfront():
+    with pytest.raises(UnschedulableError) as ei:
+        Engine([RequestSpec(0, 0.0, 100, 10)], kv_config=KvConfig(2, 16))
+    assert ei.value.request_ids == (0,)
