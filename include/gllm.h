@@ -1,0 +1,151 @@
+/*
+ * gllm.h — C-ABI of the B200 per-iteration path (libgllm.so, sm_100a).
+ *
+ * This boundary replaces the reference's two stage stand-ins and its count-only
+ * KV bookkeeping with device work:
+ *   stage_time(plan, cost)     pkg/src/tokensim/engine.py:96-100  -> gllm_stage_forward
+ *   transfer_time(plan, comm)  pkg/src/tokensim/engine.py:103-105 -> activations in
+ *                              gllm_batch.hidden, moved by NCCL send/recv (host runtime)
+ *   KvCacheState counts        pkg/src/tokensim/kvcache.py:46-95  -> device block table,
+ *                              updated by gllm_prepare_batch from the host page deltas
+ *   commit "generated += 1"    pkg/src/tokensim/engine.py:338-358 -> gllm_argmax +
+ *                              gllm_commit_tokens (sampled token becomes next input)
+ *
+ * Conventions: plain pointers and sizes only; every device pointer is caller-owned
+ * (allocated by PyTorch); nothing here calls cudaMalloc or synchronises the host;
+ * every call is stream-ordered on the stream passed in. Return value 0 = success,
+ * otherwise a GLLM_ERR_* code with a message from gllm_last_error() (thread-local).
+ * bf16 tensors are row-major; "ld" arguments are leading dimensions in elements.
+ */
+#ifndef GLLM_H_
+#define GLLM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GLLM_API __attribute__((visibility("default")))
+#else
+#define GLLM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gllm_stream_t; /* == cudaStream_t */
+
+enum {
+  GLLM_OK = 0,
+  GLLM_ERR_INVALID = 1, /* bad argument / unsupported shape */
+  GLLM_ERR_CUDA = 2     /* CUDA runtime or driver error */
+};
+
+/* Per-sequence metadata, int32 x GLLM_SEQ_FIELDS per sequence, in plan order
+ * (decodes then prefill chunks, as MicroBatchPlan, sched.py:112-133):
+ *   row      block-table / token-history row of the request
+ *   start    tokens already cached (position of the first new token)
+ *   n_new    tokens appended by this micro-batch (1 for a decode)
+ *   tok_off  first token's index in the packed token dimension
+ *   emit     index in the sampled-token output, or -1 (no token sampled) */
+#define GLLM_SEQ_FIELDS 5
+
+/* Model/stage dimensions (Llama / Qwen2 decoder, head_dim 128). */
+typedef struct gllm_dims {
+  int n_layers;     /* layers held by this stage */
+  int d_model;
+  int n_heads;
+  int n_kv_heads;
+  int head_dim;
+  int d_ff;
+  int vocab;
+  int qkv_bias;     /* 1 for Qwen2 */
+  float rms_eps;
+  int page_size;
+  int num_pages;    /* KV pages per layer */
+  int max_rows;     /* block-table / token-history rows */
+  int max_pages_per_row;
+  int max_seq_len;  /* token-history row length */
+  int max_tokens;   /* packed tokens per micro-batch (workspace sizing) */
+  int max_emit;     /* sampled rows per micro-batch (workspace sizing) */
+} gllm_dims;
+
+typedef struct gllm_layer {
+  const void* attn_norm;  /* bf16 [d] */
+  const void* w_qkv;      /* bf16 [(n_heads + 2 n_kv) * hd, d]: q | k | v rows */
+  const void* b_qkv;      /* bf16 [(n_heads + 2 n_kv) * hd] or NULL */
+  const void* w_o;        /* bf16 [d, n_heads * hd] */
+  const void* mlp_norm;   /* bf16 [d] */
+  const void* w_gate_up;  /* bf16 [2 d_ff, d]: gate rows then up rows */
+  const void* w_down;     /* bf16 [d, d_ff] */
+} gllm_layer;
+
+typedef struct gllm_stage {
+  gllm_dims dims;
+  int is_first;               /* embeds tokens, owns token history */
+  int is_last;                /* final norm, LM head, argmax */
+  const void* embed;          /* bf16 [vocab, d] (first stage) */
+  const void* final_norm;     /* bf16 [d] (last stage) */
+  const void* lm_head;        /* bf16 [vocab, d] (last stage) */
+  const gllm_layer* layers;   /* HOST array [n_layers] */
+  void* k_cache;              /* bf16 [n_layers][num_pages][n_kv][page_size][hd] */
+  void* v_cache;              /* same shape */
+  int32_t* block_table;       /* [max_rows][max_pages_per_row] */
+  int32_t* token_hist;        /* [max_rows][max_seq_len] (first stage; NULL elsewhere) */
+  const float* rope;          /* [max_seq_len][hd/2][2] (cos, sin) */
+  void* workspace;            /* >= gllm_stage_workspace_bytes(&dims) */
+  size_t workspace_bytes;
+} gllm_stage;
+
+/* One micro-batch. `meta` is ONE device int32 buffer holding, back to back:
+ *   seq_info [n_seqs][5] | attention work [n_work][2] = (seq, q_start)
+ *   | page deltas [n_deltas][3] = (row, page_index, page_id)
+ *   | prompt headers [n_prompts][3] = (row, length, token offset) | prompt tokens */
+typedef struct gllm_batch {
+  int n_seqs;
+  int n_tokens;
+  int n_emit;
+  int n_work;
+  int n_deltas;
+  int n_prompts;
+  const int32_t* meta;  /* device */
+  void* hidden;         /* bf16 [n_tokens, d]: residual stream in (non-first) / out (non-last) */
+  int32_t* sampled;     /* int32 [n_emit] (last stage) */
+  void* logits;         /* bf16 [n_emit, vocab] or NULL (workspace) */
+} gllm_batch;
+
+/* ---- library ---- */
+GLLM_API int gllm_version(void);
+GLLM_API const char* gllm_last_error(void);
+GLLM_API int gllm_attention_q_tile(int n_heads, int n_kv_heads);
+GLLM_API size_t gllm_stage_workspace_bytes(const gllm_dims* dims);
+
+/* ---- stage: one micro-batch through this stage's layers (replaces stage_time) ---- */
+GLLM_API int gllm_stage_forward(const gllm_stage* stage, const gllm_batch* batch, gllm_stream_t stream);
+/* first stage: write sampled tokens back as the next inputs (after the last stage's argmax) */
+GLLM_API int gllm_commit_tokens(const gllm_stage* stage, const gllm_batch* batch, const int32_t* sampled,
+                       gllm_stream_t stream);
+
+/* ---- individual kernels (tests, custom stages) ---- */
+GLLM_API int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N, int K,
+                   const void* bias, const void* residual, int ldr, int force_bn, int force_splits,
+                   void* workspace, size_t workspace_bytes, gllm_stream_t stream);
+GLLM_API int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,
+                 float eps, gllm_stream_t stream);
+GLLM_API int gllm_silu_mul(const void* gate_up, int d_ff, void* out, int rows, gllm_stream_t stream);
+GLLM_API int gllm_prepare_batch(const gllm_stage* stage, const gllm_batch* batch, int32_t* tok_pos, int32_t* tok_slot,
+                       int32_t* tok_id, int32_t* emit_rows, gllm_stream_t stream);
+GLLM_API int gllm_embed(const int32_t* tok_id, int n_tokens, const void* embed, int d, void* out, gllm_stream_t stream);
+GLLM_API int gllm_rope_kv_write(void* qkv, int n_tokens, int n_heads, int n_kv_heads, int head_dim, const int32_t* tok_pos,
+                       const int32_t* tok_slot, const float* rope, void* k_cache, void* v_cache, int page_size,
+                       gllm_stream_t stream);
+GLLM_API int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
+                          const int32_t* block_table, int max_pages_per_row, const void* k_cache,
+                          const void* v_cache, int n_heads, int n_kv_heads, int head_dim, int page_size, void* out,
+                          gllm_stream_t stream);
+GLLM_API int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLLM_H_ */

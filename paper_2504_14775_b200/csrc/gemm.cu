@@ -1,0 +1,371 @@
+// tcgen05 + TMA bf16 GEMM for the stage projections (QKV, O, gate-up, down, LM head).
+//
+//   C[M, N] = A[M, K] . B[N, K]^T  (+ bias[N]) (+ residual[M, N])
+//
+// A = activations (tokens x K), B = weights (out_features x K); both K-major
+// row-major bf16, exactly how the stage stores them, so no transposes.
+// One CTA owns a 128 x BN output tile (optionally a K-slice of it, split-K):
+//   warp 0  : TMA producer (one elected lane), STAGES-deep smem ring
+//   warp 1  : TMEM allocator + MMA issuer (one lane), tcgen05.mma M=128,N=BN,K=16
+//   warps 2-5: epilogue, tcgen05.ld 32 lanes x 32 cols -> bf16 (+bias/+residual)
+// Rows past M are zero-filled by TMA on load and masked on store, so decode
+// micro-batches (M = a few tokens) reuse the same kernel; they are HBM-bound on
+// the weight stream, and split-K spreads that stream over all 148 SMs.
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "gllm_internal.h"
+
+namespace gllm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int GEMM_THREADS = 192;
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+
+enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1 };
+
+template <int BN, int STAGES, int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                  int M, int N, int K, int k_blocks_per_split, bf16* __restrict__ C, int ldc,
+                  const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
+                  float* __restrict__ partial) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * BM;
+  const int total_kb = K / BK;
+  const int kb0 = blockIdx.z * k_blocks_per_split;
+  const int kb1 = min(total_kb, kb0 + k_blocks_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();  // weights stream through once per step
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        uint8_t* sb = sa + L::A_BYTES;
+        mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d(&map_a, &full[s], sa, kc, m0);
+        tma_load_2d_hint(&map_b, &full[s], sb, kc, n0, pol_w);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % STAGES;
+      const uint32_t ph = (i / STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint8_t* sa = smem + s * L::STAGE_BYTES;
+        const uint8_t* sb = sa + L::A_BYTES;
+        const uint64_t da = smem_desc_sw128(sa);
+        const uint64_t db = smem_desc_sw128(sb);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          // +32 B along K inside the swizzle atom = +2 in the 16-byte address field.
+          mma_bf16_ss(tmem_base, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
+        if (i == nkb - 1) mma_commit(tmem_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // Epilogue: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
+      tmem_ld_wait();
+      const int col = n0 + c;
+      if (row >= M || col >= N) continue;
+      if (nkb <= 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      }
+      if constexpr (MODE == EPI_PARTIAL_F32) {
+        float4* dst = reinterpret_cast<float4*>(partial + ((size_t)blockIdx.z * M + row) * N + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                               __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+      } else {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (bias != nullptr) {
+          const uint4* bp = reinterpret_cast<const uint4*>(bias + col);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u = bp[j];
+            float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), cc = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
+            v[8 * j + 0] += a.x; v[8 * j + 1] += a.y; v[8 * j + 2] += b.x; v[8 * j + 3] += b.y;
+            v[8 * j + 4] += cc.x; v[8 * j + 5] += cc.y; v[8 * j + 6] += d.x; v[8 * j + 7] += d.y;
+          }
+        }
+        if (residual != nullptr) {
+          const uint4* rp = reinterpret_cast<const uint4*>(residual + (size_t)row * ldr + col);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u = rp[j];
+            float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), cc = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
+            // round the GEMM result to bf16 first, then add: same as bf16 "x + attn(x)".
+            v[8 * j + 0] = bf2f(f2bf(v[8 * j + 0])) + a.x; v[8 * j + 1] = bf2f(f2bf(v[8 * j + 1])) + a.y;
+            v[8 * j + 2] = bf2f(f2bf(v[8 * j + 2])) + b.x; v[8 * j + 3] = bf2f(f2bf(v[8 * j + 3])) + b.y;
+            v[8 * j + 4] = bf2f(f2bf(v[8 * j + 4])) + cc.x; v[8 * j + 5] = bf2f(f2bf(v[8 * j + 5])) + cc.y;
+            v[8 * j + 6] = bf2f(f2bf(v[8 * j + 6])) + d.x; v[8 * j + 7] = bf2f(f2bf(v[8 * j + 7])) + d.y;
+          }
+        }
+        uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ldc + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                              pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, BN);
+}
+
+// Sum split-K partials [splits, M, N] fp32 and apply the epilogue; 8 columns per thread.
+__global__ void splitk_reduce(const float* __restrict__ partial, int splits, int M, int N, bf16* __restrict__ C,
+                              int ldc, const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t groups = (size_t)M * (N / 8);
+  if (idx >= groups) return;
+  const int row = (int)(idx / (N / 8));
+  const int col = (int)(idx % (N / 8)) * 8;
+  float v[8];
+  {
+    const float4* p = reinterpret_cast<const float4*>(partial + (size_t)row * N + col);
+    float4 a = p[0], b = p[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  for (int s = 1; s < splits; ++s) {
+    const float4* p = reinterpret_cast<const float4*>(partial + ((size_t)s * M + row) * N + col);
+    float4 a = p[0], b = p[1];
+    v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w; v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+  }
+  if (bias != nullptr) {
+    uint4 u = *reinterpret_cast<const uint4*>(bias + col);
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = unpack_bf16x2(w[j]);
+      v[2 * j] += f.x;
+      v[2 * j + 1] += f.y;
+    }
+  }
+  if (residual != nullptr) {
+    uint4 u = *reinterpret_cast<const uint4*>(residual + (size_t)row * ldr + col);
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = unpack_bf16x2(w[j]);
+      v[2 * j] = bf2f(f2bf(v[2 * j])) + f.x;
+      v[2 * j + 1] = bf2f(f2bf(v[2 * j + 1])) + f.y;
+    }
+  }
+  *reinterpret_cast<uint4*>(C + (size_t)row * ldc + col) =
+      make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encoder() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  int64_t rows, cols, ld;
+  int box_rows;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.ptr);
+    h ^= (size_t)k.rows * 0x9E3779B97F4A7C15ull + (size_t)k.cols * 0xC2B2AE3D27D4EB4Full + (size_t)k.ld * 31 +
+         (size_t)k.box_rows;
+    return h;
+  }
+};
+
+// bf16 [rows, cols] row-major with leading dimension ld (elements); box = 64 cols x box_rows, 128B swizzle.
+static int make_map(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, rows, cols, ld, box_rows};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return 0;
+    }
+  }
+  PFN_encodeTiled enc = get_encoder();
+  if (!enc) return set_error(GLLM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16)
+    return set_error(GLLM_ERR_INVALID, "TMA operand must be 16-byte aligned with 16-byte row pitch");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(GLLM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *out);
+  return 0;
+}
+
+template <int BN, int STAGES, int MODE>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits, int kbps,
+                       bf16* C, int ldc, const bf16* bias, const bf16* res, int ldr, float* partial,
+                       cudaStream_t st) {
+  constexpr int smem = GemmSmem<BN, STAGES>::TOTAL;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, STAGES, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
+    attr_done = true;
+  }
+  dim3 grid(N / BN, (M + BM - 1) / BM, splits);
+  gemm_bf16_tcgen05<BN, STAGES, MODE><<<grid, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, C, ldc, bias, res,
+                                                                        ldr, partial);
+  return check_launch("gemm_bf16_tcgen05");
+}
+
+int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
+              const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits,
+              void* workspace, size_t ws_bytes, cudaStream_t st) {
+  if (M <= 0) return 0;
+  if (K % BK != 0 || N % 64 != 0) return set_error(GLLM_ERR_INVALID, "gemm needs K %% 64 == 0 and N %% 64 == 0 (K=%d N=%d)", K, N);
+  if (ldc % 8 || (residual && ldr % 8)) return set_error(GLLM_ERR_INVALID, "gemm output pitch must be a multiple of 8");
+  const int num_sms = device_sm_count();
+  const int m_tiles = (M + BM - 1) / BM;
+  // Tile width: widest that still yields at least one wave of CTAs.
+  int bn = force_bn;
+  if (bn == 0) {
+    bn = 256;
+    while (bn > 64 && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
+    if (N % bn) bn = (N % 128 == 0) ? 128 : 64;
+  }
+  const int n_tiles = N / bn;
+  const int total_kb = K / BK;
+  int splits = force_splits;
+  if (splits == 0) {
+    splits = 1;
+    const long tiles = (long)n_tiles * m_tiles;
+    // Split K only when one wave is not filled (HBM-bound weight streaming for small M).
+    while (tiles * splits * 2 <= num_sms * 2 && total_kb / (splits * 2) >= 4) splits *= 2;
+    if (tiles * splits < num_sms / 2 && total_kb / (splits * 2) >= 2) splits *= 2;
+  }
+  splits = splits < 1 ? 1 : (splits > total_kb ? total_kb : splits);
+  const int kbps = (total_kb + splits - 1) / splits;
+  splits = (total_kb + kbps - 1) / kbps;
+  float* partial = nullptr;
+  if (splits > 1) {
+    size_t need = (size_t)splits * M * N * sizeof(float);
+    if (workspace == nullptr || ws_bytes < need)
+      return set_error(GLLM_ERR_INVALID, "gemm split-K workspace too small (%zu < %zu)", ws_bytes, need);
+    partial = reinterpret_cast<float*>(workspace);
+  }
+  CUtensorMap ma, mb;
+  const int a_rows = a_rows_alloc > M ? a_rows_alloc : M;
+  if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;
+  if (int rc = make_map(&mb, B, N, K, ldb, bn)) return rc;
+  int rc = 0;
+  const int mode = splits > 1 ? EPI_PARTIAL_F32 : EPI_STORE;
+#define GLLM_GEMM_CASE(BNV, ST)                                                                              \
+  if (bn == BNV) {                                                                                           \
+    rc = mode == EPI_STORE ? launch_gemm<BNV, ST, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias,    \
+                                                             residual, ldr, nullptr, st)                     \
+                           : launch_gemm<BNV, ST, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc,    \
+                                                                   nullptr, nullptr, 0, partial, st);        \
+  }
+  GLLM_GEMM_CASE(256, 4)
+  else GLLM_GEMM_CASE(128, 6) else GLLM_GEMM_CASE(64, 8) else return set_error(GLLM_ERR_INVALID, "bad BN %d", bn);
+#undef GLLM_GEMM_CASE
+  if (rc) return rc;
+  if (splits > 1) {
+    const size_t groups = (size_t)M * (N / 8);
+    const int threads = 256;
+    splitk_reduce<<<(unsigned)((groups + threads - 1) / threads), threads, 0, st>>>(partial, splits, M, N, C, ldc,
+                                                                                   bias, residual, ldr);
+    rc = check_launch("splitk_reduce");
+  }
+  return rc;
+}
+
+size_t gemm_workspace_bytes(int M, int N, int K) {
+  // Upper bound used by the stage allocator: at most 16 splits.
+  (void)K;
+  return (size_t)16 * M * N * sizeof(float);
+}
+
+}  // namespace gllm

@@ -1,0 +1,48 @@
+// Internal declarations shared by the CUDA translation units (not part of the C-ABI).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/gllm.h"
+
+namespace gllm {
+
+typedef __nv_bfloat16 bf16;
+
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* what);
+int check_launch(const char* what);
+int device_sm_count();
+
+// gemm.cu
+int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K, const bf16* bias,
+              const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits, void* workspace,
+              size_t ws_bytes, cudaStream_t st);
+size_t gemm_workspace_bytes(int M, int N, int K);
+
+// kernels.cu
+int rmsnorm(const bf16* x, int ldx, const int* row_index, const bf16* w, bf16* out, int rows, int d, float eps,
+            cudaStream_t st);
+int silu_mul(const bf16* gu, int d_ff, bf16* out, int rows, cudaStream_t st);
+int rope_kv_write(bf16* qkv, int n_tokens, int n_heads, int n_kv, int head_dim, const int* tok_pos,
+                  const int* tok_slot, const float* rope, bf16* k_cache, bf16* v_cache, int page_size,
+                  cudaStream_t st);
+int apply_batch_metadata(const int* meta, int n_deltas, int n_prompt_rows, int* block_table, int max_pages_per_row,
+                         int* token_hist, int max_seq_len, cudaStream_t st);
+int expand_tokens(const int* seq_info, int n_seqs, const int* block_table, int max_pages_per_row,
+                  const int* token_hist, int max_seq_len, int page_size, int* tok_pos, int* tok_slot, int* tok_id,
+                  int* emit_rows, const bf16* embed, int d, bf16* x_out, cudaStream_t st);
+int embed_tokens(const int* tok_id, int n_tokens, const bf16* embed, int d, bf16* out, cudaStream_t st);
+int argmax_rows(const bf16* logits, int rows, int vocab, int* out, cudaStream_t st);
+int commit_tokens(const int* seq_info, int n_seqs, const int* sampled, int* token_hist, int max_seq_len,
+                  cudaStream_t st);
+
+// attention.cu
+int attention_q_tile(int n_heads, int n_kv);
+int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
+                    int mpr, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int head_dim,
+                    int page_size, bf16* out, cudaStream_t st);
+
+}  // namespace gllm

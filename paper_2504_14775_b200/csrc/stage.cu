@@ -1,0 +1,251 @@
+// C-ABI exports (include/gllm.h) and the stage orchestrator.
+//
+// gllm_stage_forward runs one micro-batch through this stage's layers with
+// one host call (no per-kernel Python round trips): metadata apply + device
+// slot mapping, embedding (first stage), then per layer
+//   RMSNorm -> QKV GEMM(+bias) -> RoPE + paged KV write -> mixed paged attention
+//   -> O GEMM(+residual) -> RMSNorm -> gate-up GEMM -> SiLU*mul -> down GEMM(+residual)
+// and on the last stage final RMSNorm of the emitting rows -> LM head GEMM -> argmax.
+// This is the real work behind the reference's `stage_time()` stand-in
+// (`pkg/src/tokensim/engine.py:96-100`).
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "gllm_internal.h"
+
+namespace gllm {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+int set_cuda_error(cudaError_t e, const char* what) {
+  return set_error(GLLM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error(e, what);
+}
+int device_sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct StageWs {
+  bf16 *x, *h, *qkv, *attn, *gu, *act, *hf, *logits;
+  int *tok_pos, *tok_slot, *tok_id, *emit_rows;
+  float* gemm;
+  size_t gemm_bytes;
+  size_t total;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static StageWs carve(const gllm_dims& d, uint8_t* base) {
+  StageWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* p = base ? base + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  const size_t T = (size_t)d.max_tokens, E = (size_t)(d.max_emit > 0 ? d.max_emit : 1);
+  const size_t qkv_w = (size_t)(d.n_heads + 2 * d.n_kv_heads) * d.head_dim;
+  w.x = (bf16*)take(T * d.d_model * 2);
+  w.h = (bf16*)take(T * d.d_model * 2);
+  w.qkv = (bf16*)take(T * qkv_w * 2);
+  w.attn = (bf16*)take(T * (size_t)d.n_heads * d.head_dim * 2);
+  w.gu = (bf16*)take(T * 2 * (size_t)d.d_ff * 2);
+  w.act = (bf16*)take(T * (size_t)d.d_ff * 2);
+  w.hf = (bf16*)take(E * d.d_model * 2);
+  w.logits = (bf16*)take(E * (size_t)d.vocab * 2);
+  w.tok_pos = (int*)take(T * 4);
+  w.tok_slot = (int*)take(T * 4);
+  w.tok_id = (int*)take(T * 4);
+  w.emit_rows = (int*)take(E * 4);
+  // split-K partials: splits * tiles <= 2 * SMs, tile <= 128 x 256 fp32
+  w.gemm_bytes = (size_t)2 * 160 * 128 * 256 * 4;
+  w.gemm = (float*)take(w.gemm_bytes);
+  w.total = off;
+  return w;
+}
+
+struct MetaView {
+  const int *seq_info, *work, *deltas, *prompts;
+};
+static MetaView meta_view(const gllm_batch& b) {
+  MetaView v;
+  v.seq_info = b.meta;
+  v.work = v.seq_info + GLLM_SEQ_FIELDS * b.n_seqs;
+  v.deltas = v.work + 2 * b.n_work;
+  v.prompts = v.deltas + 3 * b.n_deltas;
+  return v;
+}
+
+static int prepare(const gllm_stage& S, const gllm_batch& B, int* tok_pos, int* tok_slot, int* tok_id,
+                   int* emit_rows, cudaStream_t st) {
+  const gllm_dims& d = S.dims;
+  MetaView mv = meta_view(B);
+  if (int rc = apply_batch_metadata(mv.deltas, B.n_deltas, S.token_hist ? B.n_prompts : 0, S.block_table,
+                                    d.max_pages_per_row, S.token_hist, d.max_seq_len, st))
+    return rc;
+  return expand_tokens(mv.seq_info, B.n_seqs, S.block_table, d.max_pages_per_row, S.is_first ? S.token_hist : nullptr,
+                       d.max_seq_len, d.page_size, tok_pos, tok_slot, S.is_first ? tok_id : nullptr,
+                       S.is_last ? emit_rows : nullptr, nullptr, d.d_model, nullptr, st);
+}
+
+static int validate(const gllm_stage* S, const gllm_batch* B) {
+  if (!S || !B) return set_error(GLLM_ERR_INVALID, "null stage or batch");
+  const gllm_dims& d = S->dims;
+  if (B->n_tokens > d.max_tokens) return set_error(GLLM_ERR_INVALID, "n_tokens %d > max_tokens %d", B->n_tokens, d.max_tokens);
+  if (B->n_emit > d.max_emit) return set_error(GLLM_ERR_INVALID, "n_emit %d > max_emit %d", B->n_emit, d.max_emit);
+  if (d.head_dim != 128) return set_error(GLLM_ERR_INVALID, "head_dim must be 128");
+  if (S->workspace_bytes < carve(d, nullptr).total)
+    return set_error(GLLM_ERR_INVALID, "stage workspace too small (%zu < %zu)", S->workspace_bytes, carve(d, nullptr).total);
+  if (S->is_first && (!S->embed || !S->token_hist)) return set_error(GLLM_ERR_INVALID, "first stage needs embed + token_hist");
+  if (S->is_last && (!S->final_norm || !S->lm_head)) return set_error(GLLM_ERR_INVALID, "last stage needs final_norm + lm_head");
+  if (!S->is_first && !B->hidden) return set_error(GLLM_ERR_INVALID, "non-first stage needs batch.hidden input");
+  return 0;
+}
+
+static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
+  const gllm_dims& d = S.dims;
+  StageWs w = carve(d, reinterpret_cast<uint8_t*>(S.workspace));
+  const int T = B.n_tokens;
+  const int D = d.d_model, H = d.n_heads, KV = d.n_kv_heads, HDIM = d.head_dim;
+  const int qkv_w = (H + 2 * KV) * HDIM;
+  MetaView mv = meta_view(B);
+  bf16* x = B.hidden ? reinterpret_cast<bf16*>(B.hidden) : w.x;
+  const int maxT = d.max_tokens;
+
+  if (int rc = prepare(S, B, w.tok_pos, w.tok_slot, w.tok_id, w.emit_rows, st)) return rc;
+  if (S.is_first)
+    if (int rc = embed_tokens(w.tok_id, T, reinterpret_cast<const bf16*>(S.embed), D, x, st)) return rc;
+
+  const size_t layer_kv = (size_t)d.num_pages * KV * d.page_size * HDIM;
+  for (int l = 0; l < d.n_layers; ++l) {
+    const gllm_layer& L = S.layers[l];
+    bf16* kc = reinterpret_cast<bf16*>(S.k_cache) + (size_t)l * layer_kv;
+    bf16* vc = reinterpret_cast<bf16*>(S.v_cache) + (size_t)l * layer_kv;
+    int rc;
+    if ((rc = rmsnorm(x, D, nullptr, (const bf16*)L.attn_norm, w.h, T, D, d.rms_eps, st))) return rc;
+    if ((rc = gemm_bf16(w.h, D, (const bf16*)L.w_qkv, D, w.qkv, qkv_w, T, qkv_w, D, (const bf16*)L.b_qkv, nullptr, 0,
+                        maxT, 0, 0, w.gemm, w.gemm_bytes, st)))
+      return rc;
+    if ((rc = rope_kv_write(w.qkv, T, H, KV, HDIM, w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, st))) return rc;
+    if ((rc = attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, S.block_table, d.max_pages_per_row, kc, vc, H, KV,
+                              HDIM, d.page_size, w.attn, st)))
+      return rc;
+    if ((rc = gemm_bf16(w.attn, H * HDIM, (const bf16*)L.w_o, H * HDIM, x, D, T, D, H * HDIM, nullptr, x, D, maxT, 0,
+                        0, w.gemm, w.gemm_bytes, st)))
+      return rc;
+    if ((rc = rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st))) return rc;
+    if ((rc = gemm_bf16(w.h, D, (const bf16*)L.w_gate_up, D, w.gu, 2 * d.d_ff, T, 2 * d.d_ff, D, nullptr, nullptr, 0,
+                        maxT, 0, 0, w.gemm, w.gemm_bytes, st)))
+      return rc;
+    if ((rc = silu_mul(w.gu, d.d_ff, w.act, T, st))) return rc;
+    if ((rc = gemm_bf16(w.act, d.d_ff, (const bf16*)L.w_down, d.d_ff, x, D, T, D, d.d_ff, nullptr, x, D, maxT, 0, 0,
+                        w.gemm, w.gemm_bytes, st)))
+      return rc;
+  }
+  if (S.is_last && B.n_emit > 0) {
+    bf16* logits = B.logits ? reinterpret_cast<bf16*>(B.logits) : w.logits;
+    int rc;
+    if ((rc = rmsnorm(x, D, w.emit_rows, (const bf16*)S.final_norm, w.hf, B.n_emit, D, d.rms_eps, st))) return rc;
+    if ((rc = gemm_bf16(w.hf, D, (const bf16*)S.lm_head, D, logits, d.vocab, B.n_emit, d.vocab, D, nullptr, nullptr, 0,
+                        d.max_emit, 0, 0, w.gemm, w.gemm_bytes, st)))
+      return rc;
+    if ((rc = argmax_rows(logits, B.n_emit, d.vocab, B.sampled, st))) return rc;
+    if (S.is_first)
+      if ((rc = commit_tokens(mv.seq_info, B.n_seqs, B.sampled, S.token_hist, d.max_seq_len, st))) return rc;
+  }
+  return 0;
+}
+
+}  // namespace gllm
+
+using namespace gllm;
+
+extern "C" {
+
+int gllm_version(void) { return 1; }
+const char* gllm_last_error(void) { return g_err; }
+int gllm_attention_q_tile(int n_heads, int n_kv_heads) {
+  if (n_kv_heads <= 0 || n_heads % n_kv_heads) return -1;
+  return attention_q_tile(n_heads, n_kv_heads);
+}
+size_t gllm_stage_workspace_bytes(const gllm_dims* dims) { return dims ? carve(*dims, nullptr).total : 0; }
+
+int gllm_stage_forward(const gllm_stage* stage, const gllm_batch* batch, gllm_stream_t stream) {
+  if (int rc = validate(stage, batch)) return rc;
+  return forward(*stage, *batch, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_commit_tokens(const gllm_stage* stage, const gllm_batch* batch, const int32_t* sampled,
+                       gllm_stream_t stream) {
+  if (!stage || !batch || !stage->token_hist) return set_error(GLLM_ERR_INVALID, "commit needs the first stage");
+  return commit_tokens(batch->meta, batch->n_seqs, sampled, stage->token_hist, stage->dims.max_seq_len,
+                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N, int K,
+                   const void* bias, const void* residual, int ldr, int force_bn, int force_splits, void* workspace,
+                   size_t workspace_bytes, gllm_stream_t stream) {
+  return gemm_bf16((const bf16*)A, lda, (const bf16*)B, ldb, (bf16*)C, ldc, M, N, K, (const bf16*)bias,
+                   (const bf16*)residual, ldr, M, force_bn, force_splits, workspace, workspace_bytes,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,
+                 float eps, gllm_stream_t stream) {
+  return rmsnorm((const bf16*)x, ldx, row_index, (const bf16*)weight, (bf16*)out, rows, d, eps,
+                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_silu_mul(const void* gate_up, int d_ff, void* out, int rows, gllm_stream_t stream) {
+  return silu_mul((const bf16*)gate_up, d_ff, (bf16*)out, rows, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_prepare_batch(const gllm_stage* stage, const gllm_batch* batch, int32_t* tok_pos, int32_t* tok_slot,
+                       int32_t* tok_id, int32_t* emit_rows, gllm_stream_t stream) {
+  if (!stage || !batch) return set_error(GLLM_ERR_INVALID, "null stage or batch");
+  return prepare(*stage, *batch, tok_pos, tok_slot, tok_id, emit_rows, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_embed(const int32_t* tok_id, int n_tokens, const void* embed, int d, void* out, gllm_stream_t stream) {
+  return embed_tokens(tok_id, n_tokens, (const bf16*)embed, d, (bf16*)out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_rope_kv_write(void* qkv, int n_tokens, int n_heads, int n_kv_heads, int head_dim, const int32_t* tok_pos,
+                       const int32_t* tok_slot, const float* rope, void* k_cache, void* v_cache, int page_size,
+                       gllm_stream_t stream) {
+  return rope_kv_write((bf16*)qkv, n_tokens, n_heads, n_kv_heads, head_dim, tok_pos, tok_slot, rope, (bf16*)k_cache,
+                       (bf16*)v_cache, page_size, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
+                          const int32_t* block_table, int max_pages_per_row, const void* k_cache, const void* v_cache,
+                          int n_heads, int n_kv_heads, int head_dim, int page_size, void* out, gllm_stream_t stream) {
+  return attention_paged((const bf16*)qkv, seq_info, work, n_work, block_table, max_pages_per_row,
+                         (const bf16*)k_cache, (const bf16*)v_cache, n_heads, n_kv_heads, head_dim, page_size,
+                         (bf16*)out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream) {
+  return argmax_rows((const bf16*)logits, rows, vocab, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

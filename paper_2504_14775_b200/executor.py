@@ -1,0 +1,159 @@
+"""Executors: run the engine's launched micro-batches on GPU stage workers.
+
+`LocalExecutor` keeps every stage of the pipeline in this process on one
+device (PP=1, or several stages chained back to back on one GPU for tests);
+the multi-GPU pipeline lives in `pipeline.py`. Both implement the executor
+protocol the engine calls:
+
+    launch(meta: BatchMeta)        -> enqueue the micro-batch (async, returns at once)
+    retire(seq: int)               -> wait for that batch's sampled tokens (last-stage commit)
+    on_finish(request_id, row)     -> request finished; its row may be reused
+
+Per-iteration host->device traffic is ONE int32 metadata copy from a pinned
+ring buffer (`stage.pack_batch`); device->host is the sampled token ids.
+"""
+
+from __future__ import annotations
+
+from collections import deque
+
+import numpy as np
+
+from .modelspec import ModelSpec, stage_layers
+from .stage import PackedBatch, StageWorker, default_prompt_source, pack_batch
+
+
+class _PinnedRing:
+    """Pinned host staging + device metadata buffers reused round-robin, guarded by events."""
+
+    def __init__(self, slots: int, n_ints: int, device):
+        import torch
+
+        self.host = [torch.empty(n_ints, dtype=torch.int32, pin_memory=True) for _ in range(slots)]
+        self.dev = [torch.empty(n_ints, dtype=torch.int32, device=device) for _ in range(slots)]
+        self.events = [None] * slots
+        self.i = 0
+
+    def upload(self, data: np.ndarray, stream):
+        import torch
+
+        k = self.i
+        self.i = (self.i + 1) % len(self.host)
+        if self.events[k] is not None:
+            self.events[k].synchronize()
+        n = data.size
+        if n > self.host[k].numel():
+            self.host[k] = torch.empty(2 * n, dtype=torch.int32, pin_memory=True)
+            self.dev[k] = torch.empty(2 * n, dtype=torch.int32, device=self.dev[k].device)
+        self.host[k][:n].numpy()[:] = data
+        with torch.cuda.stream(stream):
+            self.dev[k][:n].copy_(self.host[k][:n], non_blocking=True)
+        return k, self.dev[k]
+
+    def fence(self, k: int, event) -> None:
+        self.events[k] = event
+
+
+class LocalExecutor:
+    """All pipeline stages of `spec` on one GPU, executed in launch order on one stream."""
+
+    def __init__(self, spec: ModelSpec, requests, *, num_pages: int, page_size: int = 16, n_stages: int = 1,
+                 max_rows: int | None = None, max_tokens: int = 4096, max_emit: int | None = None,
+                 seed: int = 0, device="cuda", record_logits: bool = False, record_ids=None,
+                 ring_slots: int = 8):
+        import torch
+
+        self.spec = spec
+        self.device = torch.device(device)
+        self.specs = {r.id: r for r in requests}
+        max_rows = max_rows if max_rows is not None else max(1, len(requests))
+        max_seq_len = max(r.input_tokens + r.output_tokens for r in requests) + 1 if requests else 16
+        max_emit = max_emit if max_emit is not None else max(1, min(max_rows, max_tokens))
+        self.max_tokens = max_tokens
+        self.stages = [StageWorker(spec, stage_layers(spec.n_layers, n_stages, s), is_first=(s == 0),
+                                   is_last=(s == n_stages - 1), num_pages=num_pages, page_size=page_size,
+                                   max_rows=max_rows, max_seq_len=max_seq_len, max_tokens=max_tokens,
+                                   max_emit=max_emit, seed=seed, device=self.device) for s in range(n_stages)]
+        self.q_tile = self.stages[0].q_tile
+        self.prompt_source = default_prompt_source(self.specs, spec.vocab)
+        self.stream = torch.cuda.Stream(device=self.device)
+        n_ints = 16 * max_tokens + 8 * max_rows + 4 * max_seq_len
+        self.ring = _PinnedRing(ring_slots, n_ints, self.device)
+        self.hidden = torch.empty((max_tokens, spec.d_model), dtype=torch.bfloat16, device=self.device)
+        self.sampled_dev = [torch.empty(max_emit, dtype=torch.int32, device=self.device) for _ in range(ring_slots)]
+        self.sampled_host = [torch.empty(max_emit, dtype=torch.int32, pin_memory=True) for _ in range(ring_slots)]
+        self.record_logits = record_logits
+        self.record_ids = None if record_ids is None else set(record_ids)
+        self.logits_dev = (torch.empty((max_emit, spec.vocab), dtype=torch.bfloat16, device=self.device)
+                           if record_logits else None)
+        self._inflight: dict[int, tuple] = {}
+        self.outputs: dict[int, list[int]] = {}          # request id -> sampled tokens, in order
+        self.logits: list[tuple[int, int, np.ndarray]] = []  # (request id, position, fp32 logits)
+        self.timings: deque = deque()                     # (seq, start_event, end_event)
+        self.launches = 0
+
+    # -- executor protocol ----------------------------------------------------------
+
+    def launch(self, meta) -> None:
+        import torch
+
+        pb = pack_batch(meta, self.q_tile, self.prompt_source)
+        self._enqueue(pb)
+
+    def _enqueue(self, pb: PackedBatch) -> None:
+        import torch
+
+        if pb.n_tokens > self.max_tokens:
+            raise ValueError(f"micro-batch of {pb.n_tokens} tokens exceeds max_tokens={self.max_tokens}")
+        st = self.stream
+        k, meta_dev = self.ring.upload(pb.data, st)
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        sampled = self.sampled_dev[k]
+        with torch.cuda.stream(st):
+            start.record(st)
+            for w in self.stages:
+                w.forward(pb, meta_dev, hidden=self.hidden, sampled=sampled,
+                          logits=self.logits_dev if w.is_last else None, stream=st)
+            if len(self.stages) > 1 and pb.n_emit:
+                self.stages[0].commit_tokens(pb, meta_dev, sampled, stream=st)
+            end.record(st)
+            host = self.sampled_host[k]
+            if pb.n_emit:
+                host[:pb.n_emit].copy_(sampled[:pb.n_emit], non_blocking=True)
+            logits_host = None
+            if self.record_logits and pb.n_emit:
+                logits_host = self.logits_dev[:pb.n_emit].to("cpu", non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(st)
+        self.ring.fence(k, done)
+        self._inflight[pb.seq] = (pb, done, host, logits_host)
+        self.timings.append((pb.seq, start, end))
+        self.launches += 1
+
+    def retire(self, seq: int) -> list[int]:
+        pb, done, host, logits_host = self._inflight.pop(seq)
+        done.synchronize()
+        toks = host[:pb.n_emit].tolist()
+        for rid, tok in zip(pb.emit_ids, toks):
+            self.outputs.setdefault(rid, []).append(tok)
+        if logits_host is not None:
+            lg = logits_host.float().numpy()
+            for i, (rid, pos) in enumerate(zip(pb.emit_ids, pb.emit_pos)):
+                if self.record_ids is None or rid in self.record_ids:
+                    self.logits.append((rid, pos, lg[i].copy()))
+        return toks
+
+    def on_finish(self, request_id: int, row: int) -> None:
+        pass
+
+    def synchronize(self) -> None:
+        self.stream.synchronize()
+
+    def busy_ms(self) -> list[tuple[int, float]]:
+        """(seq, device ms) of every retired batch so far (CUDA events on the launch stream)."""
+        out = []
+        while self.timings and self.timings[0][0] not in self._inflight:
+            seq, a, b = self.timings.popleft()
+            out.append((seq, a.elapsed_time(b)))
+        return out

@@ -1,0 +1,146 @@
+"""Stage workers: device-resident weights, paged KV pool, block table, token history.
+
+A `StageWorker` holds one pipeline stage (a contiguous layer range) on one GPU
+and runs micro-batches through it with a single C-ABI call
+(`gllm_stage_forward`). `pack_batch` turns the engine's `BatchMeta` (the
+paper's pre-broadcast per-iteration metadata, `PAPER.md:262`) into the one
+int32 buffer the device expects (layout in include/gllm.h).
+
+HBM layout per stage (SURVEY §8(d) notation):
+  k_cache, v_cache : bf16 [L_s][num_pages][n_kv][page_size][head_dim]
+                     -> one (page, kv head) is a contiguous page_size*256 B block
+  block_table      : int32 [max_rows][ceil(max_seq_len / page_size)]
+  token_hist       : int32 [max_rows][max_seq_len]   (first stage: prompt + sampled tokens)
+  workspace        : activations for max_tokens tokens + split-K partials
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .modelspec import ModelSpec, init_embed, init_layer, rope_table
+from .workload import prompt_token_ids
+
+
+@dataclass
+class PackedBatch:
+    seq: int
+    n_seqs: int
+    n_tokens: int
+    n_emit: int
+    n_work: int
+    n_deltas: int
+    n_prompts: int
+    data: np.ndarray             # int32 packed metadata (host)
+    emit_ids: list[int]          # request id of each sampled row
+    emit_pos: list[int]          # token position each sampled row predicts
+
+
+def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
+    """Pack `engine.BatchMeta` into the device metadata layout.
+
+    `prompt_source(request_id) -> np.int32 array` supplies prompt tokens of
+    requests that got a block-table row in this batch.
+    """
+    seqs = meta.seqs
+    n = len(seqs)
+    info = np.empty((n, native.SEQ_FIELDS), dtype=np.int32)
+    emit_ids, emit_pos = [], []
+    off = 0
+    work = []
+    for i, s in enumerate(seqs):
+        e = -1
+        if s.emits:
+            e = len(emit_ids)
+            emit_ids.append(s.request_id)
+            emit_pos.append(s.start + s.n_new)
+        info[i] = (s.row, s.start, s.n_new, off, e)
+        off += s.n_new
+        for q0 in range(0, s.n_new, q_tile):
+            work.append((i, q0))
+    work_a = np.asarray(work, dtype=np.int32).reshape(-1, 2)
+    deltas = np.asarray(meta.page_deltas, dtype=np.int32).reshape(-1, 3)
+    hdrs, toks = [], []
+    toff = 0
+    for rid, row in meta.new_prompts:
+        t = np.asarray(prompt_source(rid), dtype=np.int32)
+        hdrs.append((row, len(t), toff))
+        toks.append(t)
+        toff += len(t)
+    hdr_a = np.asarray(hdrs, dtype=np.int32).reshape(-1, 3)
+    parts = [info.ravel(), work_a.ravel(), deltas.ravel(), hdr_a.ravel()] + toks
+    data = np.concatenate(parts) if parts else np.zeros(0, np.int32)
+    return PackedBatch(meta.seq, n, off, len(emit_ids), len(work_a), len(deltas), len(hdrs),
+                       data.astype(np.int32, copy=False), emit_ids, emit_pos)
+
+
+class StageWorker:
+    """One pipeline stage (layers `layers` of `spec`) resident on `device`."""
+
+    def __init__(self, spec: ModelSpec, layers: range, *, is_first: bool, is_last: bool, num_pages: int,
+                 page_size: int, max_rows: int, max_seq_len: int, max_tokens: int, max_emit: int,
+                 seed: int = 0, device="cuda"):
+        import torch
+
+        lib = native.load()
+        self.spec = spec
+        self.layer_ids = list(layers)
+        self.is_first, self.is_last = is_first, is_last
+        self.device = torch.device(device)
+        self.page_size = page_size
+        self.num_pages = num_pages
+        self.max_rows = max_rows
+        self.max_seq_len = max_seq_len
+        self.max_tokens = max_tokens
+        self.max_emit = max_emit
+        self.q_tile = lib.gllm_attention_q_tile(spec.n_heads, spec.n_kv_heads)
+        dev = self.device
+        self.layers = [init_layer(spec, l, seed, dev) for l in self.layer_ids]
+        self.embed = init_embed(spec, seed, dev, "embed") if is_first else None
+        self.final_norm = init_embed(spec, seed, dev, "final_norm") if is_last else None
+        self.lm_head = init_embed(spec, seed, dev, "lm_head") if is_last else None
+        L = len(self.layer_ids)
+        kv_shape = (L, num_pages, spec.n_kv_heads, page_size, spec.head_dim)
+        self.k_cache = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
+        self.v_cache = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
+        self.max_pages_per_row = -(-max_seq_len // page_size)
+        self.block_table = torch.zeros((max_rows, self.max_pages_per_row), dtype=torch.int32, device=dev)
+        self.token_hist = torch.zeros((max_rows, max_seq_len), dtype=torch.int32, device=dev) if is_first else None
+        self.rope = torch.from_numpy(rope_table(spec, max_seq_len)).to(dev)
+        self.dims = native.Dims(L, spec.d_model, spec.n_heads, spec.n_kv_heads, spec.head_dim, spec.d_ff, spec.vocab,
+                                int(spec.qkv_bias), spec.rms_eps, page_size, num_pages, max_rows,
+                                self.max_pages_per_row, max_seq_len, max_tokens, max_emit)
+        ws = lib.gllm_stage_workspace_bytes(C.byref(self.dims))
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
+        self._layer_arr = (native.Layer * max(L, 1))()
+        for i, w in enumerate(self.layers):
+            self._layer_arr[i] = native.Layer(*(native.ptr(w[k]) for k in
+                                                ("attn_norm", "w_qkv", "b_qkv", "w_o", "mlp_norm", "w_gate_up", "w_down")))
+        self.cstage = native.Stage(self.dims, int(is_first), int(is_last), native.ptr(self.embed),
+                                   native.ptr(self.final_norm), native.ptr(self.lm_head), self._layer_arr,
+                                   native.ptr(self.k_cache), native.ptr(self.v_cache), native.ptr(self.block_table),
+                                   native.ptr(self.token_hist), native.ptr(self.rope), native.ptr(self.workspace), ws)
+
+    def cbatch(self, pb: PackedBatch, meta_dev, hidden=None, sampled=None, logits=None) -> native.Batch:
+        return native.Batch(pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_deltas, pb.n_prompts,
+                            native.ptr(meta_dev), native.ptr(hidden), native.ptr(sampled), native.ptr(logits))
+
+    def forward(self, pb: PackedBatch, meta_dev, hidden=None, sampled=None, logits=None, stream=None) -> None:
+        """Enqueue this stage's forward for one packed micro-batch on `stream` (no host sync)."""
+        b = self.cbatch(pb, meta_dev, hidden, sampled, logits)
+        native.call("gllm_stage_forward", C.byref(self.cstage), C.byref(b), native.stream_handle(stream))
+
+    def commit_tokens(self, pb: PackedBatch, meta_dev, sampled, stream=None) -> None:
+        b = self.cbatch(pb, meta_dev)
+        native.call("gllm_commit_tokens", C.byref(self.cstage), C.byref(b), native.ptr(sampled),
+                    native.stream_handle(stream))
+
+
+def default_prompt_source(specs_by_id: dict, vocab: int):
+    def src(rid: int) -> np.ndarray:
+        return prompt_token_ids(rid, specs_by_id[rid].input_tokens, vocab)
+    return src

@@ -1,0 +1,173 @@
+"""Per-kernel parity on the B200 through the C-ABI (fp32 torch references of the same op)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib(cuda_ok):
+    from paper_2504_14775_b200 import native
+    return native
+
+
+def _rel(a, b):
+    a = a.float()
+    b = b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-12)).item()
+
+
+GEMM_SHAPES = [
+    (1, 512, 256), (7, 256, 256), (64, 1536, 256), (128, 512, 4096), (130, 4096, 4096),
+    (300, 6144, 4096), (1000, 4096, 14336), (33, 28672, 4096), (2048, 4096, 4096),
+]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_tcgen05(lib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    ws = torch.empty(160 << 20, dtype=torch.uint8, device="cuda")
+    ref = A.float() @ B.float().T
+    for bn in (0, 64, 128, 256):
+        if N % (bn or 64):
+            continue
+        for splits in (0, 1, 3):
+            C_ = torch.full((M, N), float("nan"), device="cuda").bfloat16()
+            lib.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C_.data_ptr(), N, M, N, K, None, None, 0,
+                     bn, splits, ws.data_ptr(), ws.numel(), lib.stream_handle())
+            torch.cuda.synchronize()
+            assert torch.isfinite(C_.float()).all(), (bn, splits)
+            assert _rel(C_, ref) < 8e-3, (bn, splits, _rel(C_, ref))
+    C_ = torch.empty((M, N), device="cuda").bfloat16()
+    lib.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C_.data_ptr(), N, M, N, K, bias.data_ptr(),
+             res.data_ptr(), N, 0, 0, ws.data_ptr(), ws.numel(), lib.stream_handle())
+    torch.cuda.synchronize()
+    assert _rel(C_, ref + bias.float() + res.float()) < 8e-3
+
+
+def test_rmsnorm_and_silu(lib):
+    x = torch.randn(37, 4096, device="cuda").bfloat16()
+    w = (torch.rand(4096, device="cuda") + 0.5).bfloat16()
+    out = torch.empty_like(x)
+    lib.call("gllm_rmsnorm", x.data_ptr(), 4096, None, w.data_ptr(), out.data_ptr(), 37, 4096, 1e-5, lib.stream_handle())
+    idx = torch.tensor([5, 0, 36], dtype=torch.int32, device="cuda")
+    out2 = torch.empty(3, 4096, device="cuda").bfloat16()
+    lib.call("gllm_rmsnorm", x.data_ptr(), 4096, idx.data_ptr(), w.data_ptr(), out2.data_ptr(), 3, 4096, 1e-5,
+             lib.stream_handle())
+    torch.cuda.synchronize()
+    xf = x.float()
+    ref = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-5) * w.float()
+    assert _rel(out, ref) < 5e-3
+    assert torch.equal(out2, out[[5, 0, 36]])
+    gu = torch.randn(19, 2 * 768, device="cuda").bfloat16()
+    act = torch.empty(19, 768, device="cuda").bfloat16()
+    lib.call("gllm_silu_mul", gu.data_ptr(), 768, act.data_ptr(), 19, lib.stream_handle())
+    torch.cuda.synchronize()
+    g, u = gu.float()[:, :768], gu.float()[:, 768:]
+    assert _rel(act, torch.nn.functional.silu(g) * u) < 5e-3
+
+
+def test_argmax(lib):
+    for V in (32000, 128256, 152064):
+        x = torch.randn(9, V, device="cuda").bfloat16()
+        x[3, 777] = 50.0
+        x[4, :] = 1.0       # ties -> lowest index
+        out = torch.empty(9, dtype=torch.int32, device="cuda")
+        lib.call("gllm_argmax", x.data_ptr(), 9, V, out.data_ptr(), lib.stream_handle())
+        torch.cuda.synchronize()
+        ref = x.float().argmax(-1)
+        assert out.tolist() == ref.tolist()
+        assert out[3].item() == 777 and out[4].item() == 0
+
+
+def _paged_setup(n_kv, hd, ps, ctx_lens, num_pages, seed=0):
+    """Random paged K/V; returns caches, block table and the dense per-seq K/V."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    perm = torch.randperm(num_pages, generator=g).tolist()
+    mpr = max(-(-c // ps) for c in ctx_lens) + 1
+    table = torch.zeros(len(ctx_lens), mpr, dtype=torch.int32)
+    kc = torch.randn(num_pages, n_kv, ps, hd, generator=g).bfloat16()
+    vc = torch.randn(num_pages, n_kv, ps, hd, generator=g).bfloat16()
+    dense = []
+    for i, c in enumerate(ctx_lens):
+        pages = [perm.pop() for _ in range(-(-c // ps))]
+        table[i, : len(pages)] = torch.tensor(pages)
+        idx = torch.tensor([pages[p // ps] for p in range(c)])
+        off = torch.tensor([p % ps for p in range(c)])
+        dense.append((kc[idx, :, off], vc[idx, :, off]))  # [c, n_kv, hd]
+    return kc.cuda(), vc.cuda(), table.cuda(), mpr, dense
+
+
+@pytest.mark.parametrize("n_heads,n_kv", [(32, 8), (40, 8), (64, 8), (2, 1)])
+def test_attention_mixed(lib, n_heads, n_kv):
+    hd, ps = 128, 16
+    # (start, n_new): decodes, a first chunk, a later chunk, a long decode
+    seqs = [(37, 1), (0, 45), (100, 70), (511, 1), (15, 1), (3, 200)]
+    ctx = [s + n for s, n in seqs]
+    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, ctx, num_pages=512)
+    T = sum(n for _, n in seqs)
+    qkv = torch.randn(T, (n_heads + 2 * n_kv) * hd, device="cuda").bfloat16()
+    q_tile = lib.load().gllm_attention_q_tile(n_heads, n_kv)
+    info, work, off = [], [], 0
+    for i, (s, n) in enumerate(seqs):
+        info.append([i, s, n, off, -1])
+        work += [[i, q0] for q0 in range(0, n, q_tile)]
+        off += n
+    info_t = torch.tensor(info, dtype=torch.int32, device="cuda")
+    work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
+    out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
+    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), table.data_ptr(),
+             mpr, kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
+    torch.cuda.synchronize()
+    g = n_heads // n_kv
+    for i, (s, n) in enumerate(seqs):
+        o = info[i][3]
+        q = qkv[o:o + n, : n_heads * hd].float().view(n, n_heads, hd)
+        k, v = dense[i]
+        k = k.float().repeat_interleave(g, dim=1)
+        v = v.float().repeat_interleave(g, dim=1)
+        att = torch.einsum("thd,shd->hts", q.cpu(), k) / hd ** 0.5
+        qpos = torch.arange(s, s + n)[:, None]
+        kpos = torch.arange(s + n)[None, :]
+        att = att.masked_fill(kpos > qpos, float("-inf")).softmax(-1)
+        ref = torch.einsum("hts,shd->thd", att, v).reshape(n, -1)
+        assert _rel(out[o:o + n].cpu(), ref) < 1e-2, (i, s, n)
+
+
+def test_rope_kv_write(lib):
+    from paper_2504_14775_b200.modelspec import MODELS, rope_table
+    spec = MODELS["llama3-8b"]
+    H, KV, hd, ps = spec.n_heads, spec.n_kv_heads, spec.head_dim, 16
+    T = 23
+    rope = torch.from_numpy(rope_table(spec, 4096)).cuda()
+    qkv = torch.randn(T, (H + 2 * KV) * hd, device="cuda").bfloat16()
+    orig = qkv.clone()
+    pos = torch.randint(0, 4000, (T,), dtype=torch.int32, device="cuda")
+    slot = torch.randperm(64 * ps, device="cuda")[:T].to(torch.int32)
+    kc = torch.zeros(64, KV, ps, hd, device="cuda").bfloat16()
+    vc = torch.zeros_like(kc)
+    lib.call("gllm_rope_kv_write", qkv.data_ptr(), T, H, KV, hd, pos.data_ptr(), slot.data_ptr(), rope.data_ptr(),
+             kc.data_ptr(), vc.data_ptr(), ps, lib.stream_handle())
+    torch.cuda.synchronize()
+    cs = rope[pos.long()]
+    c, s = cs[..., 0][:, None, :], cs[..., 1][:, None, :]
+
+    def rot(x):
+        x1, x2 = x[..., :64], x[..., 64:]
+        return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+    of = orig.float()
+    q_ref = rot(of[:, : H * hd].view(T, H, hd))
+    k_ref = rot(of[:, H * hd:(H + KV) * hd].view(T, KV, hd))
+    v_ref = of[:, (H + KV) * hd:].view(T, KV, hd)
+    assert _rel(qkv[:, : H * hd].view(T, H, hd), q_ref) < 5e-3
+    pg, off = (slot // ps).long(), (slot % ps).long()
+    assert _rel(kc[pg, :, off], k_ref) < 5e-3
+    assert torch.equal(vc[pg, :, off], v_ref.bfloat16())
