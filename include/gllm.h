@@ -112,7 +112,18 @@ typedef struct gllm_batch {
   void* hidden;         /* bf16 [n_tokens, d]: residual stream in (non-first) / out (non-last) */
   int32_t* sampled;     /* int32 [n_emit] (last stage) */
   void* logits;         /* bf16 [n_emit, vocab] or NULL (workspace) */
+  const int32_t* host_seq_info; /* optional HOST copy of seq_info (profiler byte/FLOP accounting) */
 } gllm_batch;
+
+/* Profiler record: one kernel class, aggregated over the launches captured between
+ * gllm_profile_begin and gllm_profile_end (CUDA events on the launching stream). */
+typedef struct gllm_profile_entry {
+  char name[32];
+  int launches;
+  double total_ms;   /* sum of per-launch event durations */
+  double flops;      /* algorithmic FLOPs (sum over launches) */
+  double bytes;      /* algorithmic DRAM bytes (sum over launches) */
+} gllm_profile_entry;
 
 /* ---- library ---- */
 GLLM_API int gllm_version(void);
@@ -144,6 +155,12 @@ GLLM_API int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, con
                           const void* v_cache, int n_heads, int n_kv_heads, int head_dim, int page_size, void* out,
                           gllm_stream_t stream);
 GLLM_API int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream);
+
+/* ---- measurement ---- */
+GLLM_API unsigned long long gllm_launch_count(void); /* kernels launched by this library so far */
+GLLM_API int gllm_profile_begin(void);
+/* synchronises the recorded events; fills up to max_entries, sets *n_entries */
+GLLM_API int gllm_profile_end(gllm_profile_entry* out, int max_entries, int* n_entries);
 
 #ifdef __cplusplus
 }

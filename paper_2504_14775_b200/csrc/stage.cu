@@ -10,8 +10,11 @@
 // (`pkg/src/tokensim/engine.py:96-100`).
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
+#include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "gllm_internal.h"
@@ -30,9 +33,56 @@ int set_error(int code, const char* fmt, ...) {
 int set_cuda_error(cudaError_t e, const char* what) {
   return set_error(GLLM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
+static std::atomic<unsigned long long> g_launches{0};
+
 int check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : set_cuda_error(e, what);
+}
+
+// ------------------------------------------------------------------ profiler
+// Kernel classes of the stage forward; each capture = (class, start/end event, algorithmic FLOPs, bytes).
+enum ProfCat {
+  P_META, P_EMBED, P_RMSNORM, P_GEMM_QKV, P_ROPE_KV, P_ATTN, P_GEMM_O, P_GEMM_GU, P_SILU, P_GEMM_DOWN,
+  P_GEMM_LM, P_ARGMAX, P_COMMIT, P_NCAT
+};
+static const char* kProfNames[P_NCAT] = {"metadata", "embed", "rmsnorm", "gemm_qkv", "rope_kv_write",
+                                          "attention", "gemm_o", "gemm_gate_up", "silu_mul", "gemm_down",
+                                          "gemm_lm_head", "argmax", "commit_tokens"};
+struct ProfRec {
+  int cat;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_pool;
+static size_t g_pool_next = 0;
+
+static cudaEvent_t pool_event() {
+  if (g_pool_next == g_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_next++];
+}
+
+template <typename F>
+static int prof_call(int cat, double flops, double bytes, cudaStream_t st, F&& fn) {
+  if (!g_prof_on) return fn();
+  cudaEvent_t a = pool_event(), b = pool_event();
+  cudaEventRecord(a, st);
+  int rc = fn();
+  cudaEventRecord(b, st);
+  g_prof.push_back({cat, a, b, flops, bytes});
+  return rc;
+}
+
+static double gemm_bytes(double M, double N, double K, bool residual, bool bias) {
+  return 2.0 * (M * K + N * K + M * N) + (residual ? 2.0 * M * N : 0.0) + (bias ? 2.0 * N : 0.0);
 }
 int device_sm_count() {
   static int n = 0;
@@ -131,9 +181,23 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
   bf16* x = B.hidden ? reinterpret_cast<bf16*>(B.hidden) : w.x;
   const int maxT = d.max_tokens;
 
-  if (int rc = prepare(S, B, w.tok_pos, w.tok_slot, w.tok_id, w.emit_rows, st)) return rc;
+  // Algorithmic attention work of this batch (profiler only; needs the host seq_info copy).
+  double att_flops = 0, att_bytes = 0;
+  if (g_prof_on && B.host_seq_info) {
+    for (int i = 0; i < B.n_seqs; ++i) {
+      const int32_t* si = B.host_seq_info + GLLM_SEQ_FIELDS * i;
+      const double start = si[1], n = si[2];
+      att_bytes += (start + n) * KV * HDIM * 2.0 * 2.0 + n * H * HDIM * 2.0 * 2.0;
+      att_flops += 4.0 * H * HDIM * (n * start + n * (n + 1) / 2.0);
+    }
+  }
+  const double Td = T, Dd = D, Fd = d.d_ff, Qd = qkv_w, Od = (double)H * HDIM;
+  if (int rc = prof_call(P_META, 0, 0, st, [&] { return prepare(S, B, w.tok_pos, w.tok_slot, w.tok_id, w.emit_rows, st); }))
+    return rc;
   if (S.is_first)
-    if (int rc = embed_tokens(w.tok_id, T, reinterpret_cast<const bf16*>(S.embed), D, x, st)) return rc;
+    if (int rc = prof_call(P_EMBED, 0, 4.0 * Td * Dd, st,
+                           [&] { return embed_tokens(w.tok_id, T, reinterpret_cast<const bf16*>(S.embed), D, x, st); }))
+      return rc;
 
   const size_t layer_kv = (size_t)d.num_pages * KV * d.page_size * HDIM;
   for (int l = 0; l < d.n_layers; ++l) {
@@ -141,36 +205,63 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
     bf16* kc = reinterpret_cast<bf16*>(S.k_cache) + (size_t)l * layer_kv;
     bf16* vc = reinterpret_cast<bf16*>(S.v_cache) + (size_t)l * layer_kv;
     int rc;
-    if ((rc = rmsnorm(x, D, nullptr, (const bf16*)L.attn_norm, w.h, T, D, d.rms_eps, st))) return rc;
-    if ((rc = gemm_bf16(w.h, D, (const bf16*)L.w_qkv, D, w.qkv, qkv_w, T, qkv_w, D, (const bf16*)L.b_qkv, nullptr, 0,
-                        maxT, 0, 0, w.gemm, w.gemm_bytes, st)))
+    if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
+                        [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.attn_norm, w.h, T, D, d.rms_eps, st); })))
       return rc;
-    if ((rc = rope_kv_write(w.qkv, T, H, KV, HDIM, w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, st))) return rc;
-    if ((rc = attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, S.block_table, d.max_pages_per_row, kc, vc, H, KV,
-                              HDIM, d.page_size, w.attn, st)))
+    if ((rc = prof_call(P_GEMM_QKV, 2.0 * Td * Qd * Dd, gemm_bytes(Td, Qd, Dd, false, L.b_qkv != nullptr), st, [&] {
+           return gemm_bf16(w.h, D, (const bf16*)L.w_qkv, D, w.qkv, qkv_w, T, qkv_w, D, (const bf16*)L.b_qkv, nullptr,
+                            0, maxT, 0, 0, w.gemm, w.gemm_bytes, st);
+         })))
       return rc;
-    if ((rc = gemm_bf16(w.attn, H * HDIM, (const bf16*)L.w_o, H * HDIM, x, D, T, D, H * HDIM, nullptr, x, D, maxT, 0,
-                        0, w.gemm, w.gemm_bytes, st)))
+    if ((rc = prof_call(P_ROPE_KV, 0, Td * (Qd + Od) * 2.0 + Td * 2.0 * KV * HDIM * 2.0, st, [&] {
+           return rope_kv_write(w.qkv, T, H, KV, HDIM, w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, st);
+         })))
       return rc;
-    if ((rc = rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st))) return rc;
-    if ((rc = gemm_bf16(w.h, D, (const bf16*)L.w_gate_up, D, w.gu, 2 * d.d_ff, T, 2 * d.d_ff, D, nullptr, nullptr, 0,
-                        maxT, 0, 0, w.gemm, w.gemm_bytes, st)))
+    if ((rc = prof_call(P_ATTN, att_flops, att_bytes, st, [&] {
+           return attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, S.block_table, d.max_pages_per_row, kc, vc,
+                                  H, KV, HDIM, d.page_size, w.attn, st);
+         })))
       return rc;
-    if ((rc = silu_mul(w.gu, d.d_ff, w.act, T, st))) return rc;
-    if ((rc = gemm_bf16(w.act, d.d_ff, (const bf16*)L.w_down, d.d_ff, x, D, T, D, d.d_ff, nullptr, x, D, maxT, 0, 0,
-                        w.gemm, w.gemm_bytes, st)))
+    if ((rc = prof_call(P_GEMM_O, 2.0 * Td * Dd * Od, gemm_bytes(Td, Dd, Od, true, false), st, [&] {
+           return gemm_bf16(w.attn, H * HDIM, (const bf16*)L.w_o, H * HDIM, x, D, T, D, H * HDIM, nullptr, x, D, maxT,
+                            0, 0, w.gemm, w.gemm_bytes, st);
+         })))
+      return rc;
+    if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
+                        [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st); })))
+      return rc;
+    if ((rc = prof_call(P_GEMM_GU, 2.0 * Td * 2 * Fd * Dd, gemm_bytes(Td, 2 * Fd, Dd, false, false), st, [&] {
+           return gemm_bf16(w.h, D, (const bf16*)L.w_gate_up, D, w.gu, 2 * d.d_ff, T, 2 * d.d_ff, D, nullptr, nullptr,
+                            0, maxT, 0, 0, w.gemm, w.gemm_bytes, st);
+         })))
+      return rc;
+    if ((rc = prof_call(P_SILU, 0, 6.0 * Td * Fd, st, [&] { return silu_mul(w.gu, d.d_ff, w.act, T, st); }))) return rc;
+    if ((rc = prof_call(P_GEMM_DOWN, 2.0 * Td * Dd * Fd, gemm_bytes(Td, Dd, Fd, true, false), st, [&] {
+           return gemm_bf16(w.act, d.d_ff, (const bf16*)L.w_down, d.d_ff, x, D, T, D, d.d_ff, nullptr, x, D, maxT, 0,
+                            0, w.gemm, w.gemm_bytes, st);
+         })))
       return rc;
   }
   if (S.is_last && B.n_emit > 0) {
     bf16* logits = B.logits ? reinterpret_cast<bf16*>(B.logits) : w.logits;
+    const double E = B.n_emit, V = d.vocab;
     int rc;
-    if ((rc = rmsnorm(x, D, w.emit_rows, (const bf16*)S.final_norm, w.hf, B.n_emit, D, d.rms_eps, st))) return rc;
-    if ((rc = gemm_bf16(w.hf, D, (const bf16*)S.lm_head, D, logits, d.vocab, B.n_emit, d.vocab, D, nullptr, nullptr, 0,
-                        d.max_emit, 0, 0, w.gemm, w.gemm_bytes, st)))
+    if ((rc = prof_call(P_RMSNORM, 0, 4.0 * E * Dd, st, [&] {
+           return rmsnorm(x, D, w.emit_rows, (const bf16*)S.final_norm, w.hf, B.n_emit, D, d.rms_eps, st);
+         })))
       return rc;
-    if ((rc = argmax_rows(logits, B.n_emit, d.vocab, B.sampled, st))) return rc;
+    if ((rc = prof_call(P_GEMM_LM, 2.0 * E * V * Dd, gemm_bytes(E, V, Dd, false, false), st, [&] {
+           return gemm_bf16(w.hf, D, (const bf16*)S.lm_head, D, logits, d.vocab, B.n_emit, d.vocab, D, nullptr,
+                            nullptr, 0, d.max_emit, 0, 0, w.gemm, w.gemm_bytes, st);
+         })))
+      return rc;
+    if ((rc = prof_call(P_ARGMAX, 0, 2.0 * E * V, st, [&] { return argmax_rows(logits, B.n_emit, d.vocab, B.sampled, st); })))
+      return rc;
     if (S.is_first)
-      if ((rc = commit_tokens(mv.seq_info, B.n_seqs, B.sampled, S.token_hist, d.max_seq_len, st))) return rc;
+      if ((rc = prof_call(P_COMMIT, 0, 0, st, [&] {
+             return commit_tokens(mv.seq_info, B.n_seqs, B.sampled, S.token_hist, d.max_seq_len, st);
+           })))
+        return rc;
   }
   return 0;
 }
@@ -246,6 +337,44 @@ int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_
 
 int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream) {
   return argmax_rows((const bf16*)logits, rows, vocab, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+unsigned long long gllm_launch_count(void) { return g_launches.load(); }
+
+int gllm_profile_begin(void) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof.clear();
+  g_pool_next = 0;
+  g_prof_on = true;
+  return 0;
+}
+
+int gllm_profile_end(gllm_profile_entry* out, int max_entries, int* n_entries) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = false;
+  gllm_profile_entry agg[P_NCAT];
+  memset(agg, 0, sizeof(agg));
+  for (const ProfRec& r : g_prof) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return set_cuda_error(e, "profile event");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    gllm_profile_entry& a = agg[r.cat];
+    a.launches += 1;
+    a.total_ms += ms;
+    a.flops += r.flops;
+    a.bytes += r.bytes;
+  }
+  int n = 0;
+  for (int c = 0; c < P_NCAT && n < max_entries; ++c) {
+    if (agg[c].launches == 0) continue;
+    out[n] = agg[c];
+    snprintf(out[n].name, sizeof(out[n].name), "%s", kProfNames[c]);
+    ++n;
+  }
+  if (n_entries) *n_entries = n;
+  g_prof.clear();
+  return 0;
 }
 
 }  // extern "C"

@@ -15,8 +15,6 @@ ring buffer (`stage.pack_batch`); device->host is the sampled token ids.
 
 from __future__ import annotations
 
-from collections import deque
-
 import numpy as np
 
 from .modelspec import ModelSpec, stage_layers
@@ -89,8 +87,10 @@ class LocalExecutor:
         self._inflight: dict[int, tuple] = {}
         self.outputs: dict[int, list[int]] = {}          # request id -> sampled tokens, in order
         self.logits: list[tuple[int, int, np.ndarray]] = []  # (request id, position, fp32 logits)
-        self.timings: deque = deque()                     # (seq, start_event, end_event)
+        self.timings: list = []                           # (seq, [(start, end) event per stage])
         self.launches = 0
+        self._epoch = None
+        self.h2d_bytes: dict[int, int] = {}              # seq -> metadata bytes copied host->device
 
     # -- executor protocol ----------------------------------------------------------
 
@@ -107,17 +107,20 @@ class LocalExecutor:
             raise ValueError(f"micro-batch of {pb.n_tokens} tokens exceeds max_tokens={self.max_tokens}")
         st = self.stream
         k, meta_dev = self.ring.upload(pb.data, st)
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
+        self.h2d_bytes[pb.seq] = int(pb.data.nbytes)
         sampled = self.sampled_dev[k]
+        evs = []
         with torch.cuda.stream(st):
-            start.record(st)
             for w in self.stages:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(st)
                 w.forward(pb, meta_dev, hidden=self.hidden, sampled=sampled,
                           logits=self.logits_dev if w.is_last else None, stream=st)
-            if len(self.stages) > 1 and pb.n_emit:
-                self.stages[0].commit_tokens(pb, meta_dev, sampled, stream=st)
-            end.record(st)
+                if w.is_last and len(self.stages) > 1 and pb.n_emit:
+                    self.stages[0].commit_tokens(pb, meta_dev, sampled, stream=st)
+                b.record(st)
+                evs.append((a, b))
             host = self.sampled_host[k]
             if pb.n_emit:
                 host[:pb.n_emit].copy_(sampled[:pb.n_emit], non_blocking=True)
@@ -128,7 +131,7 @@ class LocalExecutor:
             done.record(st)
         self.ring.fence(k, done)
         self._inflight[pb.seq] = (pb, done, host, logits_host)
-        self.timings.append((pb.seq, start, end))
+        self.timings.append((pb.seq, evs))
         self.launches += 1
 
     def retire(self, seq: int) -> list[int]:
@@ -147,13 +150,39 @@ class LocalExecutor:
     def on_finish(self, request_id: int, row: int) -> None:
         pass
 
+    # -- wall-clock driver hooks ------------------------------------------------------
+
+    def stage0_idle(self) -> bool:
+        return True   # one stream: the engine's depth gate is the only limit
+
+    def wait(self, seq: int) -> None:
+        self._inflight[seq][1].synchronize()
+
+    def mark_epoch(self) -> None:
+        import torch
+
+        self._epoch = torch.cuda.Event(enable_timing=True)
+        self._epoch.record(self.stream)
+        self.timings.clear()
+
     def synchronize(self) -> None:
         self.stream.synchronize()
 
-    def busy_ms(self) -> list[tuple[int, float]]:
-        """(seq, device ms) of every retired batch so far (CUDA events on the launch stream)."""
-        out = []
-        while self.timings and self.timings[0][0] not in self._inflight:
-            seq, a, b = self.timings.popleft()
-            out.append((seq, a.elapsed_time(b)))
+    def batch_device_ms(self) -> dict[int, float]:
+        """seq -> device ms of the whole micro-batch (all stages), from CUDA events on the launch stream."""
+        self.synchronize()
+        return {seq: evs[0][0].elapsed_time(evs[-1][1]) for seq, evs in self.timings}
+
+    def h2d_bytes_total_for(self, seqs) -> int:
+        return sum(self.h2d_bytes.get(s, 0) for s in seqs)
+
+    def stage_busy_intervals(self) -> list[list[tuple[float, float]]]:
+        """Per-stage (start, end) ms since `mark_epoch`, measured by CUDA events."""
+        self.synchronize()
+        out = [[] for _ in self.stages]
+        if self._epoch is None:
+            return out
+        for _, evs in self.timings:
+            for s, (a, b) in enumerate(evs):
+                out[s].append((self._epoch.elapsed_time(a), self._epoch.elapsed_time(b)))
         return out

@@ -21,6 +21,7 @@ EXPORTS = (
     "gllm_version", "gllm_last_error", "gllm_attention_q_tile", "gllm_stage_workspace_bytes",
     "gllm_stage_forward", "gllm_commit_tokens", "gllm_gemm_bf16", "gllm_rmsnorm", "gllm_silu_mul",
     "gllm_prepare_batch", "gllm_embed", "gllm_rope_kv_write", "gllm_attn_mixed_paged", "gllm_argmax",
+    "gllm_launch_count", "gllm_profile_begin", "gllm_profile_end",
 )
 
 
@@ -48,7 +49,12 @@ class Stage(C.Structure):
 class Batch(C.Structure):
     _fields_ = [("n_seqs", C.c_int), ("n_tokens", C.c_int), ("n_emit", C.c_int), ("n_work", C.c_int),
                 ("n_deltas", C.c_int), ("n_prompts", C.c_int), ("meta", C.c_void_p), ("hidden", C.c_void_p),
-                ("sampled", C.c_void_p), ("logits", C.c_void_p)]
+                ("sampled", C.c_void_p), ("logits", C.c_void_p), ("host_seq_info", C.c_void_p)]
+
+
+class ProfileEntry(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int), ("total_ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
 
 
 _lib = None
@@ -78,6 +84,9 @@ def load() -> C.CDLL:
         "gllm_rope_kv_write": (i, [vp, i, i, i, i, vp, vp, vp, vp, vp, i, vp]),
         "gllm_attn_mixed_paged": (i, [vp, vp, vp, i, vp, i, vp, vp, i, i, i, i, vp, vp]),
         "gllm_argmax": (i, [vp, i, i, vp, vp]),
+        "gllm_launch_count": (C.c_ulonglong, []),
+        "gllm_profile_begin": (i, []),
+        "gllm_profile_end": (i, [C.POINTER(ProfileEntry), i, C.POINTER(i)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -105,3 +114,20 @@ def stream_handle(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def profile_begin() -> None:
+    call("gllm_profile_begin")
+
+
+def profile_end() -> dict[str, dict]:
+    """Aggregated per-kernel-class CUDA-event timings captured since `profile_begin`."""
+    arr = (ProfileEntry * 64)()
+    n = C.c_int(0)
+    call("gllm_profile_end", arr, 64, C.byref(n))
+    return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
+                                   "flops": arr[i].flops, "bytes": arr[i].bytes} for i in range(n.value)}
+
+
+def launch_count() -> int:
+    return int(load().gllm_launch_count())

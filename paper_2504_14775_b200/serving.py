@@ -1,0 +1,117 @@
+"""Wall-clock serving loop: the same request state machine as `Engine`, driven by real time.
+
+Arrivals are released when the wall clock passes their `arrival_ms`; a
+micro-batch commits when its device work has finished (its sampled tokens are
+on the host), and the commit time is the request's TTFT / completion stamp.
+Scheduling keeps the reference gate (`engine.py:391-398`): fewer than `depth`
+batches in flight and stage 0 free, at most one launch per scheduling point.
+
+Per-stage busy intervals come from CUDA events on the stage streams, so
+`bubble_accounting` (`engine.py:108-125`) reports the measured pipeline
+bubble on the same definition the reference simulates.
+
+Every schedule point can be logged (`record_decisions=True`) as
+(#WP, #RD, free pages, FCFS queues, plan) for decision-replay parity against
+the reference planner.
+"""
+
+from __future__ import annotations
+
+import time
+
+from .engine import EngineCore, PipelineConfig, RawRunData
+from .errors import UnschedulableError
+from .kvcache import KvConfig
+from .metrics import IterationRecord
+from .sched import ThrottleConfig
+
+
+class ServingEngine(EngineCore):
+    def __init__(self, requests, scheduler: str = "throttle", pipeline: PipelineConfig | None = None,
+                 kv_config: KvConfig | None = None, throttle: ThrottleConfig | None = None,
+                 token_budget: int = 2048, executor=None, max_rows: int | None = None,
+                 time_scale: float = 1.0, record_decisions: bool = False):
+        if executor is None:
+            raise ValueError("ServingEngine needs a GPU executor")
+        super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget, executor, max_rows)
+        self._arrivals = sorted(requests, key=lambda s: (s.arrival_ms, s.id))
+        self._next_arrival = 0
+        self._time_scale = time_scale
+        self._t0 = None
+        self._unfinished = len(requests)
+        self.decisions: list[tuple] | None = [] if record_decisions else None
+        self.commit_log: list[tuple[int, float, int]] = []   # (seq, commit wall ms, sampled tokens)
+        self.launch_log: list[tuple[int, float]] = []        # (seq, launch wall ms)
+
+    def now_ms(self) -> float:
+        return (time.perf_counter() - self._t0) * 1000.0 * self._time_scale
+
+    def _release_arrivals(self, t: float) -> None:
+        arr = self._arrivals
+        while self._next_arrival < len(arr) and arr[self._next_arrival].arrival_ms <= t:
+            self._arrive(arr[self._next_arrival].id)
+            self._next_arrival += 1
+
+    def _decision_snapshot(self):
+        kv = self.kv
+        return (self._wp, self._rd, kv.free_pages, [k[1] for k in self._waiting], [k[1] for k in self._ready],
+                {rid: (self._reqs[rid].target - self._reqs[rid].done, kv.stored_tokens(rid))
+                 for _, rid in self._waiting},
+                {rid: kv.stored_tokens(rid) for _, rid in self._ready})
+
+    def _launch_now(self, t: float) -> bool:
+        if len(self.in_flight) >= self._pipeline.depth or not self.executor.stage0_idle():
+            return False
+        snap = self._decision_snapshot() if self.decisions is not None else None
+        plan = self._try_plan()
+        if plan is None:
+            return False
+        batch = self._make_batch(t, plan)
+        if snap is not None:
+            self.decisions.append((batch.seq, snap, list(plan.decode_ids), list(plan.prefill_chunks)))
+        self.executor.launch(batch.meta)
+        self.launch_log.append((batch.seq, t))
+        return True
+
+    def run(self, max_commits: int | None = None, on_commit=None) -> RawRunData:
+        """Serve until every request finished (or `max_commits` micro-batches committed)."""
+        ex = self.executor
+        self._t0 = time.perf_counter()
+        ex.mark_epoch()
+        commits = 0
+        while self._unfinished > 0:
+            t = self.now_ms()
+            self._release_arrivals(t)
+            if self._launch_now(t):
+                continue
+            if self.in_flight:
+                seq = min(self.in_flight)
+                ex.wait(seq)
+                t = self.now_ms()
+                self.clock = t
+                self.makespan_ms = max(self.makespan_ms, t)
+                batch = self.in_flight[seq]
+                n_out = sum(1 for s in batch.meta.seqs if s.emits)
+                self._commit(t, batch)
+                self.commit_log.append((seq, t, n_out))
+                commits += 1
+                if on_commit is not None:
+                    on_commit(seq, t, n_out)
+                if max_commits is not None and commits >= max_commits:
+                    break
+                continue
+            if self._next_arrival < len(self._arrivals):
+                wait = (self._arrivals[self._next_arrival].arrival_ms - t) / 1000.0 / self._time_scale
+                if wait > 0:
+                    time.sleep(min(wait, 0.05))
+                continue
+            stuck = tuple(sorted(rid for rid, r in self._reqs.items() if not r.finished))
+            raise UnschedulableError(f"no forward progress possible; stuck requests: {list(stuck)}", stuck)
+        ex.synchronize()
+        self._busy = ex.stage_busy_intervals()
+        return self.raw_data()
+
+    def _finish(self, r, t):  # count completions for the loop condition
+        super()._finish(r, t)
+        self._unfinished -= 1
+

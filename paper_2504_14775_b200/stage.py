@@ -126,8 +126,10 @@ class StageWorker:
                                    native.ptr(self.token_hist), native.ptr(self.rope), native.ptr(self.workspace), ws)
 
     def cbatch(self, pb: PackedBatch, meta_dev, hidden=None, sampled=None, logits=None) -> native.Batch:
+        # host seq_info view for the profiler's byte/FLOP accounting (first n_seqs*5 ints)
         return native.Batch(pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_deltas, pb.n_prompts,
-                            native.ptr(meta_dev), native.ptr(hidden), native.ptr(sampled), native.ptr(logits))
+                            native.ptr(meta_dev), native.ptr(hidden), native.ptr(sampled), native.ptr(logits),
+                            pb.data.ctypes.data)
 
     def forward(self, pb: PackedBatch, meta_dev, hidden=None, sampled=None, logits=None, stream=None) -> None:
         """Enqueue this stage's forward for one packed micro-batch on `stream` (no host sync)."""
