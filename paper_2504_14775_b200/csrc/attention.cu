@@ -11,10 +11,16 @@
 //    one key (128-bit smem reads, shuffle-reduced dot products) and each key
 //    group keeps its own online-softmax state, merged by shuffles and then
 //    across warps through shared memory. HBM-bound by design.
-//  * prefill role: up to 64 (token, head) rows of one chunk (QT = 64/G tokens x
-//    the G heads sharing the kv head), K/V staged in 32-key blocks with a
-//    cp.async double buffer, fp32 online softmax, causal mask against the
-//    chunk's own earlier tokens and its cached prefix.
+//  * prefill role (tensor cores): 128 (token, head) rows of one chunk
+//    (QT = 128/G tokens x the G heads sharing the kv head) against its cached
+//    prefix + its own earlier tokens in 64-key blocks. S = Q.K^T and O += P.V
+//    are tcgen05.mma (M=128) with S and O accumulating in TMEM; each thread
+//    owns one row (TMEM lane), so the causal mask and online softmax are
+//    thread-local. Q/K/V/P are staged in 128B-swizzled smem (K-major for Q, K,
+//    P; MN-major descriptor for V, which stays [key][dim] as the cache holds
+//    it). K blocks are double-buffered with cp.async (prefetched two blocks
+//    ahead), V single-buffered so two CTAs fit per SM; O is rescaled in TMEM only when a row's max grows by >8
+//    (log2 units), the exact "lazy rescale" form of online softmax.
 //
 // Cache layout [page][kv_head][slot][hd] (stage.py); pages resolved through the
 // device block table. Work list: int32 (seq index, q_start) pairs, host-packed.
@@ -30,16 +36,18 @@ constexpr int ATT_THREADS = 128;
 constexpr int NWARP = ATT_THREADS / 32;
 
 // ---------------------------------------------------------------- prefill role
-constexpr int KB = 32;          // keys per block
-constexpr int KPAD = HD + 8;    // bf16 row pitch in smem (conflict-free 16 B loads)
-constexpr int MAX_ROWS = 64;
-constexpr int RPW = MAX_ROWS / NWARP;  // rows per warp
+constexpr int PM = 128;        // query rows per CTA (MMA M)
+constexpr int PBK = 64;        // keys per block (MMA N of S, K of P.V)
+constexpr int TMEM_COLS = 256; // S: cols [0,64), O: cols [128,256)
+constexpr float RESCALE_TH = 8.f;
 
 struct PrefillSmem {
-  float q[MAX_ROWS][HD];
-  bf16 k[2][KB][KPAD];
-  bf16 v[2][KB][KPAD];
-  float p[MAX_ROWS][KB];
+  __align__(1024) uint8_t q[2][PM * 128];        // two 64-dim halves, SW128 K-major
+  __align__(1024) uint8_t k[2][2][PBK * 128];    // [buf][half]
+  __align__(1024) uint8_t v[2][PBK * 128];       // [half] (single buffer: keeps 2 CTAs/SM)
+  __align__(1024) uint8_t p[PM * 128];           // P [128 rows][64 keys] bf16, SW128 K-major
+  uint64_t s_bar, pv_bar;
+  uint32_t tmem_base;
 };
 
 // ---------------------------------------------------------------- decode role
@@ -267,128 +275,187 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   }
 }
 
-__device__ __forceinline__ void prefill_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok_off,
-                                             int start, int q0, int nq, const int* __restrict__ table,
+// One 128-row query tile of a prefill chunk on the tensor cores (see file header).
+template <int G>
+__device__ __forceinline__ void prefill_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok_off, int start,
+                                             int q0, int nq, const int* __restrict__ table,
                                              const bf16* __restrict__ k_cache, const bf16* __restrict__ v_cache,
                                              int n_heads, int n_kv, int kvh, int page_size, float scale_log2,
                                              bf16* __restrict__ out) {
   PrefillSmem& sm = *reinterpret_cast<PrefillSmem*>(smem_raw);
-  const int G = n_heads / n_kv;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int R = nq * G;
   const int kv_len = start + q0 + nq;
   const int qkv_w = (n_heads + 2 * n_kv) * HD;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int i = threadIdx.x; i < R * (HD / 8); i += ATT_THREADS) {
-    const int r = i / (HD / 8), c = (i % (HD / 8)) * 8;
-    const int qi = r / G, gh = r % G;
-    const uint4 u = *reinterpret_cast<const uint4*>(qkv + (size_t)(tok_off + q0 + qi) * qkv_w + (kvh * G + gh) * HD + c);
-    uint32_t a[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float2 f = unpack_bf16x2(a[j]);
-      sm.q[r][c + 2 * j] = f.x * scale_log2;
-      sm.q[r][c + 2 * j + 1] = f.y * scale_log2;
-    }
-  }
   const size_t head_stride = (size_t)page_size * HD;
-  auto load_block = [&](int blk, int buf) {
-#pragma unroll
-    for (int i = 0; i < (KB * HD / 8) / ATT_THREADS; ++i) {
-      const int idx = threadIdx.x + i * ATT_THREADS;
-      const int kk = idx >> 4, c = (idx & 15) * 8;
-      int key = blk * KB + kk;
-      if (key >= kv_len) key = kv_len - 1;  // clamp: duplicated key is masked below
-      const int page = table[key / page_size];
-      const size_t off = ((size_t)page * n_kv + kvh) * head_stride + (size_t)(key % page_size) * HD + c;
-      cp_async16(&sm.k[buf][kk][c], k_cache + off);
-      cp_async16(&sm.v[buf][kk][c], v_cache + off);
-    }
-    cp_async_commit();
-  };
+  const int nb = (kv_len + PBK - 1) / PBK;
 
-  const int rows_per_warp = (R + NWARP - 1) / NWARP;
-  float m_run[RPW], l_run[RPW], acc[RPW][4];
-#pragma unroll
-  for (int i = 0; i < RPW; ++i) {
-    m_run[i] = -FLT_MAX;
-    l_run[i] = 0.f;
-    acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  if (tid == 0) {
+    mbar_init(&sm.s_bar, 1);
+    mbar_init(&sm.pv_bar, 1);
+    fence_barrier_init();
   }
-  const int n_blocks = (kv_len + KB - 1) / KB;
-  load_block(0, 0);
-  for (int b = 0; b < n_blocks; ++b) {
-    const int buf = b & 1;
-    if (b + 1 < n_blocks) {
-      load_block(b + 1, buf ^ 1);
-      cp_async_wait<1>();
+  if (warp == 0) tmem_alloc(&sm.tmem_base, TMEM_COLS);
+
+  // Q tile -> swizzled smem (rows >= R zero-filled).
+  for (int i = tid; i < PM * 16; i += ATT_THREADS) {
+    const int r = i >> 4, c16 = i & 15, half = c16 >> 3, c = c16 & 7;
+    uint8_t* dst = sm.q[half] + sw128_off(r, c);
+    if (r < R) {
+      const int qi = r / G, gh = r % G;
+      cp_async16(dst, qkv + (size_t)(tok_off + q0 + qi) * qkv_w + (kvh * G + gh) * HD + half * 64 + c * 8);
     } else {
-      cp_async_wait<0>();
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
-    __syncthreads();
-    const int key = b * KB + lane;
-    uint32_t kr[HD / 2];
-    {
-      const uint4* kp = reinterpret_cast<const uint4*>(&sm.k[buf][lane][0]);
-#pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        uint4 u = kp[c];
-        kr[4 * c] = u.x; kr[4 * c + 1] = u.y; kr[4 * c + 2] = u.z; kr[4 * c + 3] = u.w;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      if (i >= rows_per_warp) break;
-      const int r = warp + NWARP * i;
-      if (r >= R) break;
-      const int qpos = start + q0 + r / G;
-      const float4* qp = reinterpret_cast<const float4*>(&sm.q[r][0]);
-      float s = 0.f;
-#pragma unroll
-      for (int c = 0; c < HD / 4; ++c) {
-        const float4 qv = qp[c];
-        const float2 k0 = unpack_bf16x2(kr[2 * c]), k1 = unpack_bf16x2(kr[2 * c + 1]);
-        s = fmaf(qv.x, k0.x, s); s = fmaf(qv.y, k0.y, s); s = fmaf(qv.z, k1.x, s); s = fmaf(qv.w, k1.y, s);
-      }
-      if (key > qpos || key >= kv_len) s = -FLT_MAX;
-      const float mb = warp_max(s);
-      const float m_new = fmaxf(m_run[i], mb);
-      const float p = (s == -FLT_MAX) ? 0.f : exp2f(s - m_new);
-      const float corr = (m_run[i] == -FLT_MAX) ? 0.f : exp2f(m_run[i] - m_new);
-      l_run[i] = l_run[i] * corr + warp_sum(p);
-      m_run[i] = m_new;
-      acc[i][0] *= corr; acc[i][1] *= corr; acc[i][2] *= corr; acc[i][3] *= corr;
-      sm.p[r][lane] = p;
-    }
-    __syncwarp();
-#pragma unroll 4
-    for (int j = 0; j < KB; ++j) {
-      const uint2 vv = *reinterpret_cast<const uint2*>(&sm.v[buf][j][4 * lane]);
-      const float2 v0 = unpack_bf16x2(vv.x), v1 = unpack_bf16x2(vv.y);
-#pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        if (i >= rows_per_warp) break;
-        const int r = warp + NWARP * i;
-        if (r >= R) break;
-        const float p = sm.p[r][j];
-        acc[i][0] = fmaf(p, v0.x, acc[i][0]); acc[i][1] = fmaf(p, v0.y, acc[i][1]);
-        acc[i][2] = fmaf(p, v1.x, acc[i][2]); acc[i][3] = fmaf(p, v1.y, acc[i][3]);
-      }
-    }
-    __syncthreads();
   }
+  auto load_kv = [&](const bf16* cache, uint8_t (*buf)[PBK * 128], int blk) {
+    // 64 keys x 16 chunks of 16 B; 8 per thread
 #pragma unroll
-  for (int i = 0; i < RPW; ++i) {
-    if (i >= rows_per_warp) break;
-    const int r = warp + NWARP * i;
-    if (r >= R) break;
-    const int qi = r / G, gh = r % G;
-    const float inv = l_run[i] > 0.f ? 1.f / l_run[i] : 0.f;
-    bf16* o = out + (size_t)(tok_off + q0 + qi) * (n_heads * HD) + (kvh * G + gh) * HD + 4 * lane;
-    *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16x2(acc[i][0] * inv, acc[i][1] * inv),
-                                              pack_bf16x2(acc[i][2] * inv, acc[i][3] * inv));
+    for (int j = 0; j < (PBK * 16) / ATT_THREADS; ++j) {
+      const int i = tid + j * ATT_THREADS;
+      const int kk = i >> 4, c16 = i & 15, half = c16 >> 3, c = c16 & 7;
+      int key = blk * PBK + kk;
+      if (key >= kv_len) key = kv_len - 1;  // clamped duplicate, masked in softmax
+      const int page = table[key / page_size];
+      const bf16* src = cache + ((size_t)page * n_kv + kvh) * head_stride + (size_t)(key % page_size) * HD + half * 64 + c * 8;
+      cp_async16(buf[half] + sw128_off(kk, c), src);
+    }
+  };
+  // prologue groups: [Q, K0], [K1]
+  load_kv(k_cache, sm.k[0], 0);
+  cp_async_commit();
+  if (nb > 1) load_kv(k_cache, sm.k[1], 1);
+  cp_async_commit();
+  cp_async_wait<1>();
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t t_s = tmem, t_o = tmem + 128;
+  constexpr uint32_t idesc_s = idesc_bf16_f32(PM, PBK);
+  constexpr uint32_t idesc_o = idesc_bf16_f32(PM, HD, /*b_mn_major=*/true);
+
+  auto issue_s = [&](int blk) {
+    const int b = blk & 1;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int half = kk >> 2;
+      const uint64_t da = smem_desc_sw128(sm.q[half]) + 2 * (kk & 3);
+      const uint64_t db = smem_desc_sw128(sm.k[b][half]) + 2 * (kk & 3);
+      mma_bf16_ss(t_s, da, db, idesc_s, kk > 0 ? 1u : 0u);
+    }
+    mma_commit(&sm.s_bar);
+  };
+  if (tid == 0) issue_s(0);
+
+  // per-row state: this thread owns TMEM lane / query row `tid`
+  const int row = tid;
+  const int qpos = start + q0 + (row < R ? row / G : nq - 1);
+  float m_ref = -FLT_MAX, l_sum = 0.f;
+
+  for (int j = 0; j < nb; ++j) {
+    mbar_wait(&sm.s_bar, j & 1);
+    tc_fence_after();
+    uint32_t s_raw[2][32];
+    tmem_ld_32x32b_x32(t_s + ((uint32_t)(warp * 32) << 16), s_raw[0]);
+    tmem_ld_32x32b_x32(t_s + ((uint32_t)(warp * 32) << 16) + 32, s_raw[1]);
+    tmem_ld_wait();
+    float s[PBK];
+    float mb = -FLT_MAX;
+#pragma unroll
+    for (int c = 0; c < PBK; ++c) {
+      const int kpos = j * PBK + c;
+      float x = __uint_as_float(s_raw[c >> 5][c & 31]) * scale_log2;
+      x = (kpos > qpos || kpos >= kv_len) ? -FLT_MAX : x;
+      s[c] = x;
+      mb = fmaxf(mb, x);
+    }
+    if (j > 0) mbar_wait(&sm.pv_bar, (j - 1) & 1);  // P smem free, O stable, V buffer free
+    tc_fence_after();
+    load_kv(v_cache, sm.v, j);
+    cp_async_commit();
+    // prefetch K for block j+2 into the buffer S_j just finished reading
+    if (j + 2 < nb) load_kv(k_cache, sm.k[j & 1], j + 2);
+    cp_async_commit();
+    // lazy rescale: keep the reference max unless this block exceeds it by > RESCALE_TH.
+    // The decision is per row, but tcgen05.ld/st are warp-collective, so the TMEM
+    // round trip runs for the whole warp whenever any of its rows rescales.
+    const bool grow = mb > m_ref + RESCALE_TH || m_ref == -FLT_MAX;
+    float corr = 1.f;
+    if (grow) {
+      corr = (m_ref == -FLT_MAX) ? 0.f : exp2f(m_ref - mb);
+      l_sum *= corr;
+      m_ref = mb;
+    }
+    if (j > 0 && __any_sync(0xffffffffu, grow && corr != 1.f)) {
+#pragma unroll
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t o[32];
+        const uint32_t ta = t_o + ((uint32_t)(warp * 32) << 16) + c;
+        tmem_ld_32x32b_x32(ta, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+        tmem_st_32x32b_x32(ta, o);
+      }
+      tmem_st_wait();
+    }
+    // P = exp2(s - m_ref) -> bf16, swizzled K-major row of 64 keys
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float pv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x = s[c * 8 + e];
+        pv[e] = (x == -FLT_MAX) ? 0.f : exp2f(x - m_ref);
+        l_sum += pv[e];
+      }
+      *reinterpret_cast<uint4*>(sm.p + sw128_off(row, c)) =
+          make_uint4(pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]), pack_bf16x2(pv[4], pv[5]),
+                     pack_bf16x2(pv[6], pv[7]));
+    }
+    cp_async_wait<1>();  // V_j and K_{j+1} have landed (this thread's copies); K_{j+2} may fly
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < PBK / 16; ++kk) {
+        const uint64_t da = smem_desc_sw128(sm.p) + 2 * kk;
+        const uint64_t db = smem_desc_sw128_mn(sm.v[0] + kk * 2048, PBK * 128);
+        mma_bf16_ss(t_o, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+      }
+      mma_commit(&sm.pv_bar);
+      if (j + 1 < nb) issue_s(j + 1);
+    }
   }
+  mbar_wait(&sm.pv_bar, (nb - 1) & 1);
+  tc_fence_after();
+  const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+  const int qi = row / G, gh = row % G;
+  bf16* o = out + (size_t)(tok_off + q0 + qi) * (n_heads * HD) + (kvh * G + gh) * HD;
+#pragma unroll
+  for (int c = 0; c < HD; c += 32) {
+    uint32_t r32[32];
+    tmem_ld_32x32b_x32(t_o + ((uint32_t)(warp * 32) << 16) + c, r32);  // warp-collective: all lanes
+    tmem_ld_wait();
+    if (row < R) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 8)
+        *reinterpret_cast<uint4*>(o + c + e) = make_uint4(
+            pack_bf16x2(__uint_as_float(r32[e]) * inv, __uint_as_float(r32[e + 1]) * inv),
+            pack_bf16x2(__uint_as_float(r32[e + 2]) * inv, __uint_as_float(r32[e + 3]) * inv),
+            pack_bf16x2(__uint_as_float(r32[e + 4]) * inv, __uint_as_float(r32[e + 5]) * inv),
+            pack_bf16x2(__uint_as_float(r32[e + 6]) * inv, __uint_as_float(r32[e + 7]) * inv));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
 }
+
 
 template <int G>
 __global__ void __launch_bounds__(ATT_THREADS, 2)
@@ -396,7 +463,8 @@ attn_mixed_kernel(const bf16* __restrict__ qkv, const int* __restrict__ seq_info
                   const int* __restrict__ block_table, int mpr, const bf16* __restrict__ k_cache,
                   const bf16* __restrict__ v_cache, int n_heads, int n_kv, int page_size, float scale_log2,
                   bf16* __restrict__ out) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_dyn[];
+  uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   const int item = blockIdx.x;
   const int kvh = blockIdx.y;
   const int sidx = work[2 * item];
@@ -404,19 +472,19 @@ attn_mixed_kernel(const bf16* __restrict__ qkv, const int* __restrict__ seq_info
   const int* si = seq_info + 5 * sidx;
   const int row_id = si[0], start = si[1], n_new = si[2], tok_off = si[3];
   const int* table = block_table + (size_t)row_id * mpr;
-  const int QT = MAX_ROWS / G;
-  const int nq = min(QT, n_new - q0);
-  if (nq == 1 && page_size <= 16) {
+  if (n_new == 1) {
     constexpr int LPK = G <= 4 ? 8 : 16;
     decode_role<G, LPK>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, k_cache, v_cache, n_heads, n_kv, kvh,
                         page_size, scale_log2, out);
   } else {
-    prefill_role(smem_raw, qkv, tok_off, start, q0, nq, table, k_cache, v_cache, n_heads, n_kv, kvh, page_size,
-                 scale_log2, out);
+    const int nq = min(PM / G, n_new - q0);
+    prefill_role<G>(smem_raw, qkv, tok_off, start, q0, nq, table, k_cache, v_cache, n_heads, n_kv, kvh, page_size,
+                    scale_log2, out);
   }
 }
 
-int attention_q_tile(int n_heads, int n_kv) { return MAX_ROWS / (n_heads / n_kv); }
+// Query tokens per prefill work item (a decode, n_new == 1, is always one item).
+int attention_q_tile(int n_heads, int n_kv) { return PM / (n_heads / n_kv); }
 
 template <int G>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
@@ -425,12 +493,12 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_mixed_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)ATT_SMEM);
+                                         (int)ATT_SMEM + 1024);
     if (e != cudaSuccess) return set_cuda_error(e, "attention smem attribute");
     attr = true;
   }
   dim3 grid(n_work, n_kv);
-  attn_mixed_kernel<G><<<grid, ATT_THREADS, ATT_SMEM, st>>>(qkv, seq_info, work, block_table, mpr, k_cache, v_cache,
+  attn_mixed_kernel<G><<<grid, ATT_THREADS, ATT_SMEM + 1024, st>>>(qkv, seq_info, work, block_table, mpr, k_cache, v_cache,
                                                             n_heads, n_kv, page_size, scale_log2, out);
   return check_launch("attention_mixed");
 }
@@ -441,6 +509,7 @@ int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n
   if (n_work <= 0) return 0;
   if (head_dim != HD) return set_error(GLLM_ERR_INVALID, "attention supports head_dim 128 only (got %d)", head_dim);
   if (n_heads % n_kv) return set_error(GLLM_ERR_INVALID, "bad GQA grouping");
+  if (page_size < 1 || page_size > 16) return set_error(GLLM_ERR_INVALID, "page_size must be in [1, 16]");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
   switch (n_heads / n_kv) {
     case 1: return launch_attn<1>(qkv, seq_info, work, n_work, block_table, mpr, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);

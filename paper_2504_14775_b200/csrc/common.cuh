@@ -153,6 +153,35 @@ GLLM_DEVICE void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 GLLM_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+GLLM_DEVICE void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+GLLM_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, MN-major, 128-byte swizzle: 64-element MN atoms `lbo` bytes
+// apart, 8-row K groups 1024 B apart (canonical ((8,8,m),(8,k)) layout of the PTX ISA).
+GLLM_DEVICE uint64_t smem_desc_sw128_mn(const void* base, uint32_t lbo) {
+  uint64_t addr = smem_u32(base);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Byte offset of 16-byte chunk `c` (0..7) of row `r` in a 128B-swizzled tile of 128-byte rows.
+GLLM_DEVICE uint32_t sw128_off(int r, int c) { return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)); }
+
 // Shared-memory matrix descriptor, K-major, 128-byte swizzle: 8-row core groups 1024 B apart.
 GLLM_DEVICE uint64_t smem_desc_sw128(const void* base) {
   uint64_t addr = smem_u32(base);
@@ -165,11 +194,12 @@ GLLM_DEVICE uint64_t smem_desc_sw128(const void* base) {
   return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both operands K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, A K-major, B K-major (or MN-major).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool b_mn_major = false) {
   return (1u << 4)                      // c_format = F32
          | (1u << 7)                    // a_format = BF16
          | (1u << 10)                   // b_format = BF16
+         | ((b_mn_major ? 1u : 0u) << 16)  // b_major
          | ((uint32_t)(N >> 3) << 17)   // N
          | ((uint32_t)(M >> 4) << 24);  // M
 }

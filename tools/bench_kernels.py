@@ -1,0 +1,112 @@
+"""Kernel microbenchmarks at the bench's shapes (CUDA events, warm, L2 flushed between reps).
+
+    python tools/bench_kernels.py [--only attn|gemm]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2504_14775_b200 import native  # noqa: E402
+
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json"))) \
+    if os.path.exists("MEASURED_PEAKS.json") else {"hbm_gbs": 6554.2, "bf16_tflops": 1644.5}
+FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+
+def timeit(fn, reps=10):
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        FLUSH.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16):
+    hd = 128
+    ctx = [s + n for s, n in seqs]
+    pages_per = [-(-c // ps) for c in ctx]
+    num_pages = sum(pages_per) + 8
+    mpr = max(pages_per) + 1
+    perm = torch.randperm(num_pages)
+    table = torch.zeros(len(seqs), mpr, dtype=torch.int32)
+    k = 0
+    for i, p in enumerate(pages_per):
+        table[i, :p] = perm[k:k + p]
+        k += p
+    table = table.cuda()
+    kc = torch.randn(num_pages, n_kv, ps, hd, device="cuda").bfloat16()
+    vc = torch.randn_like(kc)
+    T = sum(n for _, n in seqs)
+    qkv = torch.randn(T, (n_heads + 2 * n_kv) * hd, device="cuda").bfloat16()
+    out = torch.empty(T, n_heads * hd, device="cuda").bfloat16()
+    qt = native.load().gllm_attention_q_tile(n_heads, n_kv)
+    info, work, off = [], [], 0
+    for i, (s, n) in enumerate(seqs):
+        info.append([i, s, n, off, -1])
+        work += [[i, q0] for q0 in range(0, n, qt)]
+        off += n
+    info = torch.tensor(info, dtype=torch.int32, device="cuda")
+    work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
+    st = native.stream_handle()
+    fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work),
+                             table.data_ptr(), mpr, kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), st)
+    ms = timeit(fn)
+    kv_bytes = sum(ctx) * n_kv * hd * 2 * 2 + T * n_heads * hd * 2 * 2
+    flops = sum(4 * n_heads * hd * (n * s + n * (n + 1) / 2) for s, n in seqs)
+    print(json.dumps({"kernel": "attention", "case": name, "ms": round(ms, 4), "GB/s": round(kv_bytes / ms / 1e6, 1),
+                      "hbm_frac": round(kv_bytes / ms / 1e6 / PEAK["hbm_gbs"], 3), "TFLOP/s": round(flops / ms / 1e9, 1)}))
+
+
+def gemm_case(M, N, K, bn=0, splits=0):
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(N, K, device="cuda").bfloat16()
+    C = torch.empty(M, N, device="cuda").bfloat16()
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    st = native.stream_handle()
+    fn = lambda: native.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, None, None, 0,
+                             bn, splits, ws.data_ptr(), ws.numel(), st)
+    ms = timeit(fn)
+    fl = 2 * M * N * K
+    by = 2 * (M * K + N * K + M * N)
+    ref = timeit(lambda: torch.matmul(A, B.T))
+    print(json.dumps({"kernel": "gemm", "M": M, "N": N, "K": K, "bn": bn, "splits": splits, "ms": round(ms, 4),
+                      "TFLOP/s": round(fl / ms / 1e9, 1), "GB/s": round(by / ms / 1e6, 1),
+                      "cublas_ms": round(ref, 4), "cublas_TFLOP/s": round(fl / ref / 1e9, 1)}))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--case", default="")
+    a = ap.parse_args()
+    if a.case:
+        _orig = attn_case
+        attn_case = lambda name, *x, **k: _orig(name, *x, **k) if name == a.case else None
+    torch.manual_seed(0)
+    if a.only in ("", "attn"):
+        attn_case("decode800_ctx500", [(500, 1)] * 800)
+        attn_case("decode64_ctx2000", [(2000, 1)] * 64)
+        attn_case("decode8_ctx8000", [(8000, 1)] * 8)
+        attn_case("prefill_4x300_from0", [(0, 300)] * 4)
+        attn_case("prefill_chunk512_after1500", [(1500, 512)])
+        attn_case("mixed_bench", [(500, 1)] * 800 + [(0, 300)] * 3 + [(200, 300)] * 1)
+        attn_case("decode256_qwen", [(600, 1)] * 256, n_heads=40)
+        attn_case("decode128_70b", [(4000, 1)] * 128, n_heads=64)
+    if a.only in ("", "gemm"):
+        for M in (1, 16, 64, 128, 256, 512, 1024, 2048, 2944):
+            for N, K in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)):
+                gemm_case(M, N, K)
+        gemm_case(1000, 128256, 4096)
