@@ -196,7 +196,8 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
 #pragma unroll
     for (int kk = 0; kk < MAXK; ++kk) {
       const int t = kk * KPI + grp;
-      if (t >= page_size) continue;
+      // Slots past kv_len hold stale pool bytes (possibly NaN/Inf): skip, never multiply by 0.
+      if (t >= keys_here) continue;
       const bf16* vr = vp + t * HD + sub * DPL;
       float vv[DPL];
 #pragma unroll

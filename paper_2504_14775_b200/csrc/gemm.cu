@@ -49,8 +49,10 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * BM;
+  // M-tiles vary fastest: the CTAs of one wave share each weight (B) tile through L2, so
+  // the weight matrix streams from HBM ~once per GEMM instead of once per M-tile.
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
   const int total_kb = K / BK;
   const int kb0 = blockIdx.z * k_blocks_per_split;
   const int kb1 = min(total_kb, kb0 + k_blocks_per_split);
@@ -294,7 +296,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_done = true;
   }
-  dim3 grid(N / BN, (M + BM - 1) / BM, splits);
+  dim3 grid((M + BM - 1) / BM, N / BN, splits);
   gemm_bf16_tcgen05<BN, STAGES, MODE><<<grid, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, C, ldc, bias, res,
                                                                         ldr, partial);
   return check_launch("gemm_bf16_tcgen05");

@@ -12,6 +12,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -80,6 +82,40 @@ static int prof_call(int cat, double flops, double bytes, cudaStream_t st, F&& f
   g_prof.push_back({cat, a, b, flops, bytes});
   return rc;
 }
+
+// ---------------------------------------------------------------- debug: GLLM_CHECK_FINITE=1
+__global__ void count_nonfinite_kernel(const bf16* __restrict__ x, size_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = __bfloat162float(x[i]);
+    if (!isfinite(v)) ++c;
+  }
+  if (c) atomicAdd(out, c);
+}
+static bool check_finite_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("GLLM_CHECK_FINITE");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+static int check_finite(const bf16* x, size_t n, const char* what, int layer, cudaStream_t st) {
+  static unsigned long long* d = nullptr;
+  if (!d) cudaMalloc(&d, sizeof(*d));
+  cudaMemsetAsync(d, 0, sizeof(*d), st);
+  count_nonfinite_kernel<<<256, 256, 0, st>>>(x, n, d);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  if (h) {
+    fprintf(stderr, "[gllm] non-finite output: %s layer %d: %llu of %zu\n", what, layer, h, n);
+    return set_error(GLLM_ERR_CUDA, "non-finite output of %s (layer %d)", what, layer);
+  }
+  return 0;
+}
+#define GLLM_CHECK(ptr, n, what, layer) \
+  if (check_finite_enabled()) { if (int rc_ = check_finite((ptr), (n), (what), (layer), st)) return rc_; }
 
 static double gemm_bytes(double M, double N, double K, bool residual, bool bias) {
   return 2.0 * (M * K + N * K + M * N) + (residual ? 2.0 * M * N : 0.0) + (bias ? 2.0 * N : 0.0);
@@ -194,6 +230,7 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
   const double Td = T, Dd = D, Fd = d.d_ff, Qd = qkv_w, Od = (double)H * HDIM;
   if (int rc = prof_call(P_META, 0, 0, st, [&] { return prepare(S, B, w.tok_pos, w.tok_slot, w.tok_id, w.emit_rows, st); }))
     return rc;
+  GLLM_CHECK(x, (size_t)T * D * (S.is_first ? 0 : 1), "stage_input", -1);
   if (S.is_first)
     if (int rc = prof_call(P_EMBED, 0, 4.0 * Td * Dd, st,
                            [&] { return embed_tokens(w.tok_id, T, reinterpret_cast<const bf16*>(S.embed), D, x, st); }))
@@ -213,20 +250,24 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
                             0, maxT, 0, 0, w.gemm, w.gemm_bytes, st);
          })))
       return rc;
+    GLLM_CHECK(w.qkv, (size_t)T * qkv_w, "gemm_qkv", l);
     if ((rc = prof_call(P_ROPE_KV, 0, Td * (Qd + Od) * 2.0 + Td * 2.0 * KV * HDIM * 2.0, st, [&] {
            return rope_kv_write(w.qkv, T, H, KV, HDIM, w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, st);
          })))
       return rc;
+    GLLM_CHECK(w.qkv, (size_t)T * qkv_w, "rope_kv_write", l);
     if ((rc = prof_call(P_ATTN, att_flops, att_bytes, st, [&] {
            return attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, S.block_table, d.max_pages_per_row, kc, vc,
                                   H, KV, HDIM, d.page_size, w.attn, st);
          })))
       return rc;
+    GLLM_CHECK(w.attn, (size_t)T * H * HDIM, "attention", l);
     if ((rc = prof_call(P_GEMM_O, 2.0 * Td * Dd * Od, gemm_bytes(Td, Dd, Od, true, false), st, [&] {
            return gemm_bf16(w.attn, H * HDIM, (const bf16*)L.w_o, H * HDIM, x, D, T, D, H * HDIM, nullptr, x, D, maxT,
                             0, 0, w.gemm, w.gemm_bytes, st);
          })))
       return rc;
+    GLLM_CHECK(x, (size_t)T * D, "gemm_o", l);
     if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
                         [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st); })))
       return rc;
@@ -235,12 +276,14 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
                             0, maxT, 0, 0, w.gemm, w.gemm_bytes, st);
          })))
       return rc;
+    GLLM_CHECK(w.gu, (size_t)T * 2 * d.d_ff, "gemm_gate_up", l);
     if ((rc = prof_call(P_SILU, 0, 6.0 * Td * Fd, st, [&] { return silu_mul(w.gu, d.d_ff, w.act, T, st); }))) return rc;
     if ((rc = prof_call(P_GEMM_DOWN, 2.0 * Td * Dd * Fd, gemm_bytes(Td, Dd, Fd, true, false), st, [&] {
            return gemm_bf16(w.act, d.d_ff, (const bf16*)L.w_down, d.d_ff, x, D, T, D, d.d_ff, nullptr, x, D, maxT, 0,
                             0, w.gemm, w.gemm_bytes, st);
          })))
       return rc;
+    GLLM_CHECK(x, (size_t)T * D, "gemm_down", l);
   }
   if (S.is_last && B.n_emit > 0) {
     bf16* logits = B.logits ? reinterpret_cast<bf16*>(B.logits) : w.logits;

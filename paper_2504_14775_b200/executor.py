@@ -91,6 +91,9 @@ class LocalExecutor:
         self.launches = 0
         self._epoch = None
         self.h2d_bytes: dict[int, int] = {}              # seq -> metadata bytes copied host->device
+        # Weights, block tables and token history were initialised on torch's current stream;
+        # the executor stream is non-blocking, so order it after that work once.
+        torch.cuda.synchronize(self.device)
 
     # -- executor protocol ----------------------------------------------------------
 

@@ -103,6 +103,10 @@ def _paged_setup(n_kv, hd, ps, ctx_lens, num_pages, seed=0):
         idx = torch.tensor([pages[p // ps] for p in range(c)])
         off = torch.tensor([p % ps for p in range(c)])
         dense.append((kc[idx, :, off], vc[idx, :, off]))  # [c, n_kv, hd]
+        # stale slots past the context in the last page hold garbage (NaN here): must never leak
+        if c % ps:
+            kc[pages[-1], :, c % ps:] = float("nan")
+            vc[pages[-1], :, c % ps:] = float("nan")
     return kc.cuda(), vc.cuda(), table.cuda(), mpr, dense
 
 

@@ -1,0 +1,66 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU and exports every symbol include/gllm.h declares."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2504_14775_b200 import native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "gllm.h")).read()
+    return sorted(set(re.findall(r"GLLM_API\s+[\w\s\*]+?\b(gllm_\w+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2504_14775_b200 import build
+    build.build()
+    return native.load()
+
+
+def test_exports_match_header(lib):
+    declared = _declared()
+    assert len(declared) >= 15
+    assert sorted(native.EXPORTS) == declared
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_host_only_entry_points(lib):
+    assert lib.gllm_version() >= 1
+    assert lib.gllm_attention_q_tile(32, 8) == 32     # 128 rows / G=4
+    assert lib.gllm_attention_q_tile(40, 8) == 25
+    assert lib.gllm_attention_q_tile(64, 8) == 16
+    assert lib.gllm_attention_q_tile(3, 2) == -1
+    d = native.Dims(32, 4096, 32, 8, 128, 14336, 128256, 0, 1e-5, 16, 1000, 64, 64, 1024, 3072, 1024)
+    assert lib.gllm_stage_workspace_bytes(C.byref(d)) > 3072 * 4096 * 2
+
+
+def test_errors_are_reported_not_crashing(lib):
+    # NULL stage: rejected on the host before any CUDA call
+    rc = lib.gllm_stage_forward(None, None, None)
+    assert rc == 1 and b"null" in lib.gllm_last_error()
+    with pytest.raises(native.NativeError):
+        native.call("gllm_stage_forward", None, None, None)
+
+
+def test_pack_batch_layout():
+    """Host packer: seq_info / work / deltas / prompts land where include/gllm.h says."""
+    import numpy as np
+
+    from paper_2504_14775_b200.engine import BatchMeta, SeqMeta
+    from paper_2504_14775_b200.stage import pack_batch
+    meta = BatchMeta(seq=3, seqs=[SeqMeta(7, 2, 40, 1, True), SeqMeta(9, 5, 0, 70, False), SeqMeta(4, 1, 10, 5, True)],
+                     page_deltas=np.array([[5, 0, 11], [5, 1, 12]], np.int32), new_prompts=[(9, 5)])
+    pb = pack_batch(meta, 32, lambda rid: np.arange(3, dtype=np.int32) + 100)
+    assert (pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_deltas, pb.n_prompts) == (3, 76, 2, 5, 2, 1)
+    d = pb.data
+    assert d[:15].tolist() == [2, 40, 1, 0, 0, 5, 0, 70, 1, -1, 1, 10, 5, 71, 1]
+    assert d[15:25].tolist() == [0, 0, 1, 0, 1, 32, 1, 64, 2, 0]
+    assert d[25:31].tolist() == [5, 0, 11, 5, 1, 12]
+    assert d[31:34].tolist() == [5, 3, 0] and d[34:].tolist() == [100, 101, 102]
+    assert pb.emit_ids == [7, 4] and pb.emit_pos == [41, 15]
