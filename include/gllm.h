@@ -106,6 +106,7 @@ typedef struct gllm_batch {
   int n_tokens;
   int n_emit;
   int n_work;
+  int n_prefill_work;   /* work items with more than one query token (0 => all-decode launch) */
   int n_deltas;
   int n_prompts;
   const int32_t* meta;  /* device */
@@ -151,7 +152,8 @@ GLLM_API int gllm_rope_kv_write(void* qkv, int n_tokens, int n_heads, int n_kv_h
                        const int32_t* tok_slot, const float* rope, void* k_cache, void* v_cache, int page_size,
                        gllm_stream_t stream);
 GLLM_API int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
-                          const int32_t* block_table, int max_pages_per_row, const void* k_cache,
+                          int n_prefill_work, const int32_t* block_table, int max_pages_per_row, int kv_pages,
+                          const void* k_cache,
                           const void* v_cache, int n_heads, int n_kv_heads, int head_dim, int page_size, void* out,
                           gllm_stream_t stream);
 GLLM_API int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream);

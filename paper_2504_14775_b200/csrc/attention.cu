@@ -1,16 +1,16 @@
 // Mixed-batch paged attention: chunked-prefill chunks and decodes in ONE launch.
 //
-// Work item = (sequence, q_start) x kv head (grid.y). The role is uniform per CTA:
+// Work item = (sequence, q_start) x kv head (grid.x). The role is uniform per CTA:
 //
 //  * decode role (the item has one query token): the CTA streams the sequence's
 //    K and V pages for its kv head straight from the paged cache with
 //    cp.async.bulk (the 1-D TMA engine): one (page, kv head) block is a
 //    contiguous page_size*256 B run, so each page costs two bulk copies and no
 //    address math per element. Every warp owns a 2-stage page ring guarded by
-//    mbarriers and walks pages w, w+4, ...; inside a warp LPK lanes cooperate on
-//    one key (128-bit smem reads, shuffle-reduced dot products) and each key
-//    group keeps its own online-softmax state, merged by shuffles and then
-//    across warps through shared memory. HBM-bound by design.
+//    mbarriers and walks pages w, w+4, ...; the G query heads are one 16-row
+//    HMMA tile (mma.sync m16n8k16: this GEMV-shaped work is too small for a
+//    128-row tcgen05 tile), online softmax on lane quads, warps merged through
+//    shared memory. HBM-bound by design.
 //  * prefill role (tensor cores): 128 (token, head) rows of one chunk
 //    (QT = 128/G tokens x the G heads sharing the kv head) against its cached
 //    prefix + its own earlier tokens in 64-key blocks. S = Q.K^T and O += P.V
@@ -51,14 +51,16 @@ struct PrefillSmem {
 };
 
 // ---------------------------------------------------------------- decode role
-constexpr int DEC_STAGES = 2;
+constexpr int DEC_STAGES = 3;
 constexpr int MAX_PAGE_BYTES = 16 * HD * 2;  // page_size <= 16 for the bulk ring
 struct DecodeSmem {
-  __align__(128) uint8_t kv[NWARP][DEC_STAGES][2][MAX_PAGE_BYTES];
+  union {
+    __align__(128) uint8_t kv[NWARP][DEC_STAGES][2][MAX_PAGE_BYTES];
+    float merge_acc[NWARP][8][HD];  // reused after every page has been consumed
+  };
   uint64_t full[NWARP][DEC_STAGES];
   float merge_m[NWARP][8];
   float merge_l[NWARP][8];
-  float merge_acc[NWARP][8][HD];
 };
 
 constexpr size_t ATT_SMEM = sizeof(PrefillSmem) > sizeof(DecodeSmem) ? sizeof(PrefillSmem) : sizeof(DecodeSmem);
@@ -78,146 +80,166 @@ GLLM_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* 
 }
 GLLM_DEVICE void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// G query heads share the kv head; LPK lanes cooperate on one key (DPL dims each).
-template <int G, int LPK>
+GLLM_DEVICE void mma_16816_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+GLLM_DEVICE void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+GLLM_DEVICE void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
+// Decode role: one query token, the G query heads of kv head `kvh` padded to a
+// 16-row MMA tile. Each warp streams its pages (w, w+4, ...) through a 2-stage
+// cp.async.bulk ring and per 16-key page issues 16 HMMA for S = Q.K^T and 16 for
+// O += P.V (P reused from the S accumulator registers), with the online softmax
+// on quads of lanes (one query head per quad). Warps merge through smem.
+template <int G>
 __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok, int kv_len,
-                                            const int* __restrict__ table, const bf16* __restrict__ k_cache,
-                                            const bf16* __restrict__ v_cache, int n_heads, int n_kv, int kvh,
+                                            const int* __restrict__ table, const CUtensorMap* k_map,
+                                            const CUtensorMap* v_map, int n_heads, int n_kv, int kvh,
                                             int page_size, float scale_log2, bf16* __restrict__ out) {
-  constexpr int DPL = HD / LPK;       // dims per lane (16 or 8)
-  constexpr int KPI = 32 / LPK;       // keys per warp iteration
+  static_assert(G <= 8, "decode tile holds up to 8 query heads per kv head");
+  constexpr int HALF_BYTES = 16 * 128;  // one 64-dim box of a 16-slot page (8-slot pages use half)
   DecodeSmem& sm = *reinterpret_cast<DecodeSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane % LPK, grp = lane / LPK;
+  const int qr = lane >> 2;          // fragment row = query head within the group
+  const int qc = (lane & 3) * 2;     // fragment column pair
   const int qkv_w = (n_heads + 2 * n_kv) * HD;
   const uint32_t page_bytes = (uint32_t)page_size * HD * 2;
-  const size_t head_stride = (size_t)page_size * HD;
   const int n_pages = (kv_len + page_size - 1) / page_size;
+  const int nblk = page_size / 8;    // 8-key MMA n-blocks per page (1 or 2)
 
   if (lane == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&sm.full[warp][s], 1);
     fence_barrier_init();
   }
   __syncwarp();
-
+  // One page of one kv head = page_size rows x 128 dims; two 64-dim TMA boxes per tensor,
+  // landing 128B-swizzled (row r, 16B chunk c at r*128 + ((c ^ r%8) << 4)) so the ldmatrix
+  // fragment loads below are bank-conflict free.
   auto issue = [&](int p, int s) {
-    const int page = table[p];
-    const size_t off = ((size_t)page * n_kv + kvh) * head_stride;
+    const int row0 = (table[p] * n_kv + kvh) * page_size;
     mbar_arrive_expect_tx(&sm.full[warp][s], 2 * page_bytes);
-    bulk_g2s(sm.kv[warp][s][0], k_cache + off, page_bytes, &sm.full[warp][s]);
-    bulk_g2s(sm.kv[warp][s][1], v_cache + off, page_bytes, &sm.full[warp][s]);
+    tma_load_2d(k_map, &sm.full[warp][s], sm.kv[warp][s][0], 0, row0);
+    tma_load_2d(k_map, &sm.full[warp][s], sm.kv[warp][s][0] + HALF_BYTES, 64, row0);
+    tma_load_2d(v_map, &sm.full[warp][s], sm.kv[warp][s][1], 0, row0);
+    tma_load_2d(v_map, &sm.full[warp][s], sm.kv[warp][s][1] + HALF_BYTES, 64, row0);
   };
-  // prologue: first DEC_STAGES pages of this warp in flight
   if (lane == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) {
       const int p = warp + s * NWARP;
       if (p < n_pages) issue(p, s);
     }
   }
-
-  // q slice of the G heads for this lane's dims, fp32, pre-scaled for exp2.
-  float q[G][DPL];
-  const bf16* qrow = qkv + (size_t)tok * qkv_w + (kvh * G) * HD + sub * DPL;
+  // Q as A fragments (rows >= G are zero), 8 k-steps of 16 dims.
+  uint32_t qa[8][4];
+  {
+    const bf16* qrow = qkv + (size_t)tok * qkv_w + (kvh * G + qr) * HD;
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-#pragma unroll
-    for (int c = 0; c < DPL; c += 8) {
-      const uint4 u = *reinterpret_cast<const uint4*>(qrow + h * HD + c);
-      const uint32_t a[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 f = unpack_bf16x2(a[j]);
-        q[h][c + 2 * j] = f.x * scale_log2;
-        q[h][c + 2 * j + 1] = f.y * scale_log2;
-      }
+    for (int kk = 0; kk < 8; ++kk) {
+      const bool live = qr < G;
+      qa[kk][0] = live ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + qc) : 0u;
+      qa[kk][1] = 0u;
+      qa[kk][2] = live ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + qc) : 0u;
+      qa[kk][3] = 0u;
     }
   }
-  float m[G], l[G], acc[G][DPL];
+  float o[16][4];
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    m[h] = -FLT_MAX;
-    l[h] = 0.f;
-#pragma unroll
-    for (int d = 0; d < DPL; ++d) acc[h][d] = 0.f;
-  }
+  for (int nb = 0; nb < 16; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+  float m_run = -FLT_MAX, l_run = 0.f;   // row qr's state, replicated across its quad
 
   int it = 0;
   for (int p = warp; p < n_pages; p += NWARP, ++it) {
     const int s = it % DEC_STAGES;
     mbar_wait(&sm.full[warp][s], (uint32_t)((it / DEC_STAGES) & 1));
-    const bf16* kp = reinterpret_cast<const bf16*>(sm.kv[warp][s][0]);
-    const bf16* vp = reinterpret_cast<const bf16*>(sm.kv[warp][s][1]);
+    uint8_t* kp = sm.kv[warp][s][0];
+    uint8_t* vp = sm.kv[warp][s][1];
     const int keys_here = min(page_size, kv_len - p * page_size);
-    // scores for this lane group's keys of the page
-    constexpr int MAXK = 16 / KPI > 0 ? 16 / KPI : 1;  // keys per lane group for page_size 16
-    float sc[MAXK][G];
+    if (keys_here < page_size) {
+      // stale slots past kv_len may hold NaN/Inf bytes: zero their V rows (0 * NaN would poison O)
+      for (int i = lane; i < (page_size - keys_here) * 16; i += 32)
+        *reinterpret_cast<uint4*>(vp + (i & 8 ? HALF_BYTES : 0) + (keys_here + i / 16) * 128 + (i & 7) * 16) =
+            make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    // ---- S = Q K^T : per 8-key n-block, 8 k-steps
+    float sc[2][4];
 #pragma unroll
-    for (int kk = 0; kk < MAXK; ++kk) {
-      const int t = kk * KPI + grp;
-      const bool valid = t < keys_here;
-      float part[G];
+    for (int nb = 0; nb < 2; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
 #pragma unroll
-      for (int h = 0; h < G; ++h) part[h] = 0.f;
-      if (t < page_size) {
-        const bf16* kr = kp + t * HD + sub * DPL;
+    for (int kk2 = 0; kk2 < 8; kk2 += 2) {
 #pragma unroll
-        for (int c = 0; c < DPL; c += 8) {
-          const uint4 u = *reinterpret_cast<const uint4*>(kr + c);
-          const uint32_t a[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 f = unpack_bf16x2(a[j]);
-#pragma unroll
-            for (int h = 0; h < G; ++h) part[h] = fmaf(q[h][c + 2 * j + 1], f.y, fmaf(q[h][c + 2 * j], f.x, part[h]));
-          }
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-#pragma unroll
-        for (int o = LPK / 2; o > 0; o >>= 1) part[h] += __shfl_xor_sync(0xffffffffu, part[h], o);
-        sc[kk][h] = valid ? part[h] : -FLT_MAX;
+      for (int nb = 0; nb < 2; ++nb) {
+        if (nb >= nblk) break;
+        // 4 matrices: (keys nb*8.., dims kk2*16 + {0,8}) and (.., dims (kk2+1)*16 + {0,8})
+        const int j = lane >> 3, r = lane & 7;
+        const int c = (kk2 & 3) * 2 + j;              // 16B chunk within the 64-dim half
+        uint32_t kb[4];
+        ldsm_x4(kb, kp + (kk2 >> 2) * HALF_BYTES + (nb * 8 + r) * 128 + ((c ^ r) << 4));
+        mma_16816_bf16(sc[nb], qa[kk2], kb[0], kb[1]);
+        mma_16816_bf16(sc[nb], qa[kk2 + 1], kb[2], kb[3]);
       }
     }
-    // one rescale per page, then accumulate P.V for this group's keys
+    // ---- online softmax for row qr over this page's keys (4 per lane in its quad)
+    float mx = m_run;
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      float mx = m[h];
+    for (int nb = 0; nb < 2; ++nb) {
 #pragma unroll
-      for (int kk = 0; kk < MAXK; ++kk) mx = fmaxf(mx, sc[kk][h]);
-      const float corr = (m[h] == -FLT_MAX) ? 0.f : exp2f(m[h] - mx);
-      m[h] = mx;
-      l[h] *= corr;
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) acc[h][d] *= corr;
-#pragma unroll
-      for (int kk = 0; kk < MAXK; ++kk) sc[kk][h] = (sc[kk][h] == -FLT_MAX) ? 0.f : exp2f(sc[kk][h] - mx);
+      for (int e = 0; e < 2; ++e) {
+        const int key = nb * 8 + qc + e;
+        const bool valid = nb < nblk && key < keys_here;
+        const float x = sc[nb][e] * scale_log2;
+        sc[nb][e] = valid ? x : -FLT_MAX;
+        mx = fmaxf(mx, sc[nb][e]);
+      }
     }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float corr = (m_run == -FLT_MAX) ? 0.f : exp2f(m_run - mx);
+    m_run = mx;
+    float psum = 0.f;
+    uint32_t pa[4];
 #pragma unroll
-    for (int kk = 0; kk < MAXK; ++kk) {
-      const int t = kk * KPI + grp;
-      // Slots past kv_len hold stale pool bytes (possibly NaN/Inf): skip, never multiply by 0.
-      if (t >= keys_here) continue;
-      const bf16* vr = vp + t * HD + sub * DPL;
-      float vv[DPL];
+    for (int nb = 0; nb < 2; ++nb) {
+      const float p0 = sc[nb][0] == -FLT_MAX ? 0.f : exp2f(sc[nb][0] - mx);
+      const float p1 = sc[nb][1] == -FLT_MAX ? 0.f : exp2f(sc[nb][1] - mx);
+      psum += p0 + p1;
+      pa[nb * 2] = pack_bf16x2(p0, p1);  // a0a1 (keys 0-7) / a4a5 (keys 8-15) of row qr
+      pa[nb * 2 + 1] = 0u;               // rows 8-15 are padding
+    }
+    psum += __shfl_xor_sync(0xffffffffu, psum, 1);
+    psum += __shfl_xor_sync(0xffffffffu, psum, 2);
+    l_run = l_run * corr + psum;
+    if (__any_sync(0xffffffffu, corr != 1.f)) {
 #pragma unroll
-      for (int c = 0; c < DPL; c += 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(vr + c);
-        const uint32_t a[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16x2(a[j]);
-          vv[c + 2 * j] = f.x;
-          vv[c + 2 * j + 1] = f.y;
-        }
+      for (int nb = 0; nb < 16; ++nb) {
+        o[nb][0] *= corr;
+        o[nb][1] *= corr;
       }
+    }
+    // ---- O += P V : A = P (row qr; keys 0-7 in reg 0, 8-15 in reg 2), B = V via ldmatrix.trans
+    const uint32_t a_frag[4] = {pa[0], pa[1], nblk > 1 ? pa[2] : 0u, pa[3]};
 #pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const float pr = sc[kk][h];
-        l[h] += pr;
-#pragma unroll
-        for (int d = 0; d < DPL; ++d) acc[h][d] = fmaf(pr, vv[d], acc[h][d]);
-      }
+    for (int nb = 0; nb < 16; nb += 2) {
+      const int j = lane >> 3, r = lane & 7;
+      const int key = (j & 1) * 8 + r;
+      const int dblk = nb + (j >> 1);                 // 8-dim block 0..15
+      uint32_t vb[4];
+      ldsm_x4_t(vb, vp + (dblk >> 3) * HALF_BYTES + (key < page_size ? key : 0) * 128 + (((dblk & 7) ^ r) << 4));
+      if (nblk < 2) { vb[1] = 0u; vb[3] = 0u; }
+      mma_16816_bf16(o[nb], a_frag, vb[0], vb[1]);
+      mma_16816_bf16(o[nb + 1], a_frag, vb[2], vb[3]);
     }
     __syncwarp();
     const int pn = p + DEC_STAGES * NWARP;
@@ -226,36 +248,18 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
       issue(pn, s);
     }
   }
-
-  // merge the KPI key groups of this warp (lanes sub, sub+LPK, ...)
-#pragma unroll
-  for (int o = LPK; o < 32; o <<= 1) {
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const float mo = __shfl_xor_sync(0xffffffffu, m[h], o);
-      const float lo = __shfl_xor_sync(0xffffffffu, l[h], o);
-      const float mn = fmaxf(m[h], mo);
-      const float ca = (m[h] == -FLT_MAX) ? 0.f : exp2f(m[h] - mn);
-      const float cb = (mo == -FLT_MAX) ? 0.f : exp2f(mo - mn);
-      l[h] = l[h] * ca + lo * cb;
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) {
-        const float ao = __shfl_xor_sync(0xffffffffu, acc[h][d], o);
-        acc[h][d] = acc[h][d] * ca + ao * cb;
-      }
-      m[h] = mn;
+  // ---- merge the 4 warps through smem (rows < G only); the ring is reused, so all
+  // warps must be done with their pages first
+  __syncthreads();
+  if (qr < G) {
+    if ((lane & 3) == 0) {
+      sm.merge_m[warp][qr] = m_run;
+      sm.merge_l[warp][qr] = l_run;
     }
-  }
-  // across warps through shared memory
-  if (grp == 0) {
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      if (sub == 0) {
-        sm.merge_m[warp][h] = m[h];
-        sm.merge_l[warp][h] = l[h];
-      }
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) sm.merge_acc[warp][h][sub * DPL + d] = acc[h][d];
+    for (int nb = 0; nb < 16; ++nb) {
+      sm.merge_acc[warp][qr][nb * 8 + qc] = o[nb][0];
+      sm.merge_acc[warp][qr][nb * 8 + qc + 1] = o[nb][1];
     }
   }
   __syncthreads();
@@ -275,6 +279,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
     out[(size_t)tok * (n_heads * HD) + (kvh * G + h) * HD + d] = f2bf(den > 0.f ? num / den : 0.f);
   }
 }
+
 
 // One 128-row query tile of a prefill chunk on the tensor cores (see file header).
 template <int G>
@@ -458,26 +463,30 @@ __device__ __forceinline__ void prefill_role(uint8_t* smem_raw, const bf16* __re
 }
 
 
-template <int G>
+// MIXED: decode and prefill CTAs in one launch. DECODE_ONLY: an all-decode micro-batch
+// (no prefill smem / TMEM / registers reserved, so more CTAs stay resident per SM).
+enum AttnRoles { ROLES_MIXED = 0, ROLES_DECODE_ONLY = 1 };
+
+template <int G, int ROLES>
 __global__ void __launch_bounds__(ATT_THREADS, 2)
-attn_mixed_kernel(const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
+attn_mixed_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
+                  const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
                   const int* __restrict__ block_table, int mpr, const bf16* __restrict__ k_cache,
                   const bf16* __restrict__ v_cache, int n_heads, int n_kv, int page_size, float scale_log2,
                   bf16* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  const int item = blockIdx.x;
-  const int kvh = blockIdx.y;
+  const int kvh = blockIdx.x;   // kv heads fastest: a work item's CTAs launch together
+  const int item = blockIdx.y;
   const int sidx = work[2 * item];
   const int q0 = work[2 * item + 1];
   const int* si = seq_info + 5 * sidx;
   const int row_id = si[0], start = si[1], n_new = si[2], tok_off = si[3];
   const int* table = block_table + (size_t)row_id * mpr;
-  if (n_new == 1) {
-    constexpr int LPK = G <= 4 ? 8 : 16;
-    decode_role<G, LPK>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, k_cache, v_cache, n_heads, n_kv, kvh,
-                        page_size, scale_log2, out);
-  } else {
+  if (ROLES == ROLES_DECODE_ONLY || n_new == 1) {
+    decode_role<G>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh,
+                   page_size, scale_log2, out);
+  } else if constexpr (ROLES == ROLES_MIXED) {
     const int nq = min(PM / G, n_new - q0);
     prefill_role<G>(smem_raw, qkv, tok_off, start, q0, nq, table, k_cache, v_cache, n_heads, n_kv, kvh, page_size,
                     scale_log2, out);
@@ -487,37 +496,56 @@ attn_mixed_kernel(const bf16* __restrict__ qkv, const int* __restrict__ seq_info
 // Query tokens per prefill work item (a decode, n_new == 1, is always one item).
 int attention_q_tile(int n_heads, int n_kv) { return PM / (n_heads / n_kv); }
 
-template <int G>
+template <int G, int ROLES>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
-                       int mpr, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
+                       int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
                        float scale_log2, bf16* out, cudaStream_t st) {
+  constexpr size_t smem = (ROLES == ROLES_DECODE_ONLY ? sizeof(DecodeSmem) : ATT_SMEM) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_mixed_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)ATT_SMEM + 1024);
+    cudaError_t e = cudaFuncSetAttribute(attn_mixed_kernel<G, ROLES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e, "attention smem attribute");
+    // all of the unified L1/smem as shared memory: two CTAs (8 streaming warps) per SM
+    e = cudaFuncSetAttribute(attn_mixed_kernel<G, ROLES>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return set_cuda_error(e, "attention carveout attribute");
     attr = true;
   }
-  dim3 grid(n_work, n_kv);
-  attn_mixed_kernel<G><<<grid, ATT_THREADS, ATT_SMEM + 1024, st>>>(qkv, seq_info, work, block_table, mpr, k_cache, v_cache,
-                                                            n_heads, n_kv, page_size, scale_log2, out);
+  // the paged cache viewed as a 2-D [pages*kv_heads*page_size, 128] bf16 tensor for the decode TMA boxes
+  CUtensorMap km, vm;
+  if (int rc = make_tma_map_2d(&km, k_cache, (int64_t)kv_pages * n_kv * page_size, HD, HD, page_size)) return rc;
+  if (int rc = make_tma_map_2d(&vm, v_cache, (int64_t)kv_pages * n_kv * page_size, HD, HD, page_size)) return rc;
+  dim3 grid(n_kv, n_work);
+  attn_mixed_kernel<G, ROLES><<<grid, ATT_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, block_table, mpr, k_cache,
+                                                              v_cache, n_heads, n_kv, page_size, scale_log2, out);
   return check_launch("attention_mixed");
 }
 
-int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
-                    int mpr, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int head_dim,
-                    int page_size, bf16* out, cudaStream_t st) {
+template <int G>
+static int launch_attn_g(bool decode_only, const bf16* qkv, const int* seq_info, const int* work, int n_work,
+                         const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads,
+                         int n_kv, int page_size, float scale_log2, bf16* out, cudaStream_t st) {
+  return decode_only ? launch_attn<G, ROLES_DECODE_ONLY>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache,
+                                                         n_heads, n_kv, page_size, scale_log2, out, st)
+                     : launch_attn<G, ROLES_MIXED>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache,
+                                                   n_heads, n_kv, page_size, scale_log2, out, st);
+}
+
+int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, int n_prefill_work,
+                    const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache,
+                    int n_heads, int n_kv, int head_dim, int page_size, bf16* out, cudaStream_t st) {
   if (n_work <= 0) return 0;
   if (head_dim != HD) return set_error(GLLM_ERR_INVALID, "attention supports head_dim 128 only (got %d)", head_dim);
   if (n_heads % n_kv) return set_error(GLLM_ERR_INVALID, "bad GQA grouping");
-  if (page_size < 1 || page_size > 16) return set_error(GLLM_ERR_INVALID, "page_size must be in [1, 16]");
+  if (page_size != 8 && page_size != 16) return set_error(GLLM_ERR_INVALID, "page_size must be 8 or 16");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
+  const bool dec = n_prefill_work == 0;
   switch (n_heads / n_kv) {
-    case 1: return launch_attn<1>(qkv, seq_info, work, n_work, block_table, mpr, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 2: return launch_attn<2>(qkv, seq_info, work, n_work, block_table, mpr, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 4: return launch_attn<4>(qkv, seq_info, work, n_work, block_table, mpr, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 5: return launch_attn<5>(qkv, seq_info, work, n_work, block_table, mpr, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 8: return launch_attn<8>(qkv, seq_info, work, n_work, block_table, mpr, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    case 1: return launch_attn_g<1>(dec, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    case 2: return launch_attn_g<2>(dec, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    case 4: return launch_attn_g<4>(dec, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    case 5: return launch_attn_g<5>(dec, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    case 8: return launch_attn_g<8>(dec, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
     default: return set_error(GLLM_ERR_INVALID, "unsupported GQA group %d", n_heads / n_kv);
   }
 }

@@ -284,6 +284,10 @@ static int make_map(CUtensorMap* out, const void* ptr, int64_t rows, int64_t col
   return 0;
 }
 
+int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  return make_map(out, ptr, rows, cols, ld, box_rows);
+}
+
 template <int BN, int STAGES, int MODE>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits, int kbps,
                        bf16* C, int ldc, const bf16* bias, const bf16* res, int ldr, float* partial,

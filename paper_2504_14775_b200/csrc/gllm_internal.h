@@ -1,5 +1,6 @@
 // Internal declarations shared by the CUDA translation units (not part of the C-ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -21,6 +22,8 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, 
               const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits, void* workspace,
               size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int M, int N, int K);
+// bf16 [rows, cols] (leading dim ld) as a TMA map with 64-col x box_rows boxes, 128B swizzle (cached)
+int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 
 // kernels.cu
 int rmsnorm(const bf16* x, int ldx, const int* row_index, const bf16* w, bf16* out, int rows, int d, float eps,
@@ -41,8 +44,8 @@ int commit_tokens(const int* seq_info, int n_seqs, const int* sampled, int* toke
 
 // attention.cu
 int attention_q_tile(int n_heads, int n_kv);
-int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
-                    int mpr, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int head_dim,
+int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, int n_prefill_work,
+                    const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int head_dim,
                     int page_size, bf16* out, cudaStream_t st);
 
 }  // namespace gllm

@@ -257,8 +257,8 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
       return rc;
     GLLM_CHECK(w.qkv, (size_t)T * qkv_w, "rope_kv_write", l);
     if ((rc = prof_call(P_ATTN, att_flops, att_bytes, st, [&] {
-           return attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, S.block_table, d.max_pages_per_row, kc, vc,
-                                  H, KV, HDIM, d.page_size, w.attn, st);
+           return attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, B.n_prefill_work, S.block_table,
+                                  d.max_pages_per_row, d.num_pages, kc, vc, H, KV, HDIM, d.page_size, w.attn, st);
          })))
       return rc;
     GLLM_CHECK(w.attn, (size_t)T * H * HDIM, "attention", l);
@@ -371,9 +371,12 @@ int gllm_rope_kv_write(void* qkv, int n_tokens, int n_heads, int n_kv_heads, int
 }
 
 int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
-                          const int32_t* block_table, int max_pages_per_row, const void* k_cache, const void* v_cache,
-                          int n_heads, int n_kv_heads, int head_dim, int page_size, void* out, gllm_stream_t stream) {
-  return attention_paged((const bf16*)qkv, seq_info, work, n_work, block_table, max_pages_per_row,
+                          int n_prefill_work, const int32_t* block_table, int max_pages_per_row, int kv_pages,
+                          const void* k_cache,
+                          const void* v_cache, int n_heads, int n_kv_heads, int head_dim, int page_size, void* out,
+                          gllm_stream_t stream) {
+  return attention_paged((const bf16*)qkv, seq_info, work, n_work, n_prefill_work, block_table, max_pages_per_row,
+                         kv_pages,
                          (const bf16*)k_cache, (const bf16*)v_cache, n_heads, n_kv_heads, head_dim, page_size,
                          (bf16*)out, reinterpret_cast<cudaStream_t>(stream));
 }

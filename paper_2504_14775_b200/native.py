@@ -48,7 +48,7 @@ class Stage(C.Structure):
 
 class Batch(C.Structure):
     _fields_ = [("n_seqs", C.c_int), ("n_tokens", C.c_int), ("n_emit", C.c_int), ("n_work", C.c_int),
-                ("n_deltas", C.c_int), ("n_prompts", C.c_int), ("meta", C.c_void_p), ("hidden", C.c_void_p),
+                ("n_prefill_work", C.c_int), ("n_deltas", C.c_int), ("n_prompts", C.c_int), ("meta", C.c_void_p), ("hidden", C.c_void_p),
                 ("sampled", C.c_void_p), ("logits", C.c_void_p), ("host_seq_info", C.c_void_p)]
 
 
@@ -82,7 +82,7 @@ def load() -> C.CDLL:
         "gllm_prepare_batch": (i, [C.POINTER(Stage), C.POINTER(Batch), vp, vp, vp, vp, vp]),
         "gllm_embed": (i, [vp, i, vp, i, vp, vp]),
         "gllm_rope_kv_write": (i, [vp, i, i, i, i, vp, vp, vp, vp, vp, i, vp]),
-        "gllm_attn_mixed_paged": (i, [vp, vp, vp, i, vp, i, vp, vp, i, i, i, i, vp, vp]),
+        "gllm_attn_mixed_paged": (i, [vp, vp, vp, i, i, vp, i, i, vp, vp, i, i, i, i, vp, vp]),
         "gllm_argmax": (i, [vp, i, i, vp, vp]),
         "gllm_launch_count": (C.c_ulonglong, []),
         "gllm_profile_begin": (i, []),

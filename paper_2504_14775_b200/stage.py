@@ -33,6 +33,7 @@ class PackedBatch:
     n_tokens: int
     n_emit: int
     n_work: int
+    n_prefill_work: int
     n_deltas: int
     n_prompts: int
     data: np.ndarray             # int32 packed metadata (host)
@@ -51,7 +52,7 @@ def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
     info = np.empty((n, native.SEQ_FIELDS), dtype=np.int32)
     emit_ids, emit_pos = [], []
     off = 0
-    work = []
+    work_pf, work_dec = [], []
     for i, s in enumerate(seqs):
         e = -1
         if s.emits:
@@ -60,9 +61,14 @@ def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
             emit_pos.append(s.start + s.n_new)
         info[i] = (s.row, s.start, s.n_new, off, e)
         off += s.n_new
-        for q0 in range(0, s.n_new, q_tile):
-            work.append((i, q0))
-    work_a = np.asarray(work, dtype=np.int32).reshape(-1, 2)
+        if s.n_new == 1:
+            work_dec.append((i, 0))
+        else:
+            work_pf.extend((i, q0) for q0 in range(0, s.n_new, q_tile))
+    # Heavy prefill tiles first: CTAs launch in work order, so they overlap the decode stream
+    # instead of forming the tail of the launch.
+    n_prefill_work = len(work_pf)
+    work_a = np.asarray(work_pf + work_dec, dtype=np.int32).reshape(-1, 2)
     deltas = np.asarray(meta.page_deltas, dtype=np.int32).reshape(-1, 3)
     hdrs, toks = [], []
     toff = 0
@@ -74,7 +80,7 @@ def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
     hdr_a = np.asarray(hdrs, dtype=np.int32).reshape(-1, 3)
     parts = [info.ravel(), work_a.ravel(), deltas.ravel(), hdr_a.ravel()] + toks
     data = np.concatenate(parts) if parts else np.zeros(0, np.int32)
-    return PackedBatch(meta.seq, n, off, len(emit_ids), len(work_a), len(deltas), len(hdrs),
+    return PackedBatch(meta.seq, n, off, len(emit_ids), len(work_a), n_prefill_work, len(deltas), len(hdrs),
                        data.astype(np.int32, copy=False), emit_ids, emit_pos)
 
 
@@ -127,7 +133,7 @@ class StageWorker:
 
     def cbatch(self, pb: PackedBatch, meta_dev, hidden=None, sampled=None, logits=None) -> native.Batch:
         # host seq_info view for the profiler's byte/FLOP accounting (first n_seqs*5 ints)
-        return native.Batch(pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_deltas, pb.n_prompts,
+        return native.Batch(pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_prefill_work, pb.n_deltas, pb.n_prompts,
                             native.ptr(meta_dev), native.ptr(hidden), native.ptr(sampled), native.ptr(logits),
                             pb.data.ctypes.data)
 

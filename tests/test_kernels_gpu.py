@@ -128,8 +128,8 @@ def test_attention_mixed(lib, n_heads, n_kv):
     info_t = torch.tensor(info, dtype=torch.int32, device="cuda")
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
     out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
-    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), table.data_ptr(),
-             mpr, kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
+    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), sum(1 for i, _ in work if seqs[i][1] > 1), table.data_ptr(),
+             mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
     torch.cuda.synchronize()
     g = n_heads // n_kv
     for i, (s, n) in enumerate(seqs):
@@ -175,3 +175,28 @@ def test_rope_kv_write(lib):
     pg, off = (slot // ps).long(), (slot % ps).long()
     assert _rel(kc[pg, :, off], k_ref) < 5e-3
     assert torch.equal(vc[pg, :, off], v_ref.bfloat16())
+
+
+@pytest.mark.parametrize("n_heads,n_kv", [(32, 8), (64, 8), (40, 8)])
+def test_attention_decode_only_launch(lib, n_heads, n_kv):
+    """All-decode micro-batch: the decode-only instantiation (no prefill resources) must agree too."""
+    hd, ps = 128, 16
+    seqs = [(c, 1) for c in (0, 1, 15, 16, 17, 300, 1023, 2047)]
+    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, [s + 1 for s, _ in seqs], num_pages=512, seed=3)
+    T = len(seqs)
+    qkv = torch.randn(T, (n_heads + 2 * n_kv) * hd, device="cuda").bfloat16()
+    info = torch.tensor([[i, s, 1, i, -1] for i, (s, _) in enumerate(seqs)], dtype=torch.int32, device="cuda")
+    work = torch.tensor([[i, 0] for i in range(T)], dtype=torch.int32, device="cuda")
+    out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
+    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work.data_ptr(), T, 0, table.data_ptr(), mpr, kc.shape[0],
+             kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
+    torch.cuda.synchronize()
+    g = n_heads // n_kv
+    for i, (s, _) in enumerate(seqs):
+        q = qkv[i, : n_heads * hd].float().view(n_heads, hd)
+        k, v = dense[i]
+        k = k.float().repeat_interleave(g, dim=1)
+        v = v.float().repeat_interleave(g, dim=1)
+        att = (torch.einsum("hd,shd->hs", q.cpu(), k) / hd ** 0.5).softmax(-1)
+        ref = torch.einsum("hs,shd->hd", att, v).reshape(-1)
+        assert _rel(out[i].cpu(), ref) < 1e-2, (i, s)

@@ -57,10 +57,10 @@ def test_pack_batch_layout():
     meta = BatchMeta(seq=3, seqs=[SeqMeta(7, 2, 40, 1, True), SeqMeta(9, 5, 0, 70, False), SeqMeta(4, 1, 10, 5, True)],
                      page_deltas=np.array([[5, 0, 11], [5, 1, 12]], np.int32), new_prompts=[(9, 5)])
     pb = pack_batch(meta, 32, lambda rid: np.arange(3, dtype=np.int32) + 100)
-    assert (pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_deltas, pb.n_prompts) == (3, 76, 2, 5, 2, 1)
+    assert (pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_prefill_work, pb.n_deltas, pb.n_prompts) == (3, 76, 2, 5, 4, 2, 1)
     d = pb.data
     assert d[:15].tolist() == [2, 40, 1, 0, 0, 5, 0, 70, 1, -1, 1, 10, 5, 71, 1]
-    assert d[15:25].tolist() == [0, 0, 1, 0, 1, 32, 1, 64, 2, 0]
+    assert d[15:25].tolist() == [1, 0, 1, 32, 1, 64, 2, 0, 0, 0]   # prefill tiles first, then decodes
     assert d[25:31].tolist() == [5, 0, 11, 5, 1, 12]
     assert d[31:34].tolist() == [5, 3, 0] and d[34:].tolist() == [100, 101, 102]
     assert pb.emit_ids == [7, 4] and pb.emit_pos == [41, 15]

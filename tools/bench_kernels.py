@@ -56,13 +56,14 @@ def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16):
     info, work, off = [], [], 0
     for i, (s, n) in enumerate(seqs):
         info.append([i, s, n, off, -1])
-        work += [[i, q0] for q0 in range(0, n, qt)]
+        work += [[i, q0] for q0 in range(0, n, qt)] if n > 1 else []
         off += n
+    work = work + [[i, 0] for i, (s, n) in enumerate(seqs) if n == 1]   # prefill tiles first (as the packer)
     info = torch.tensor(info, dtype=torch.int32, device="cuda")
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
     st = native.stream_handle()
-    fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work),
-                             table.data_ptr(), mpr, kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), st)
+    fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work), sum(1 for i, _ in work if seqs[i][1] > 1),
+                             table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), st)
     ms = timeit(fn)
     kv_bytes = sum(ctx) * n_kv * hd * 2 * 2 + T * n_heads * hd * 2 * 2
     flops = sum(4 * n_heads * hd * (n * s + n * (n + 1) / 2) for s, n in seqs)
