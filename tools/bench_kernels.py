@@ -34,7 +34,7 @@ def timeit(fn, reps=10):
     return ts[len(ts) // 2]
 
 
-def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16):
+def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False):
     hd = 128
     ctx = [s + n for s, n in seqs]
     pages_per = [-(-c // ps) for c in ctx]
@@ -62,7 +62,7 @@ def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16):
     info = torch.tensor(info, dtype=torch.int32, device="cuda")
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
     st = native.stream_handle()
-    fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work), sum(1 for i, _ in work if seqs[i][1] > 1),
+    fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work), max(int(force_mixed), sum(1 for i, _ in work if seqs[i][1] > 1)),
                              table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), st)
     ms = timeit(fn)
     kv_bytes = sum(ctx) * n_kv * hd * 2 * 2 + T * n_heads * hd * 2 * 2
@@ -101,6 +101,8 @@ if __name__ == "__main__":
         attn_case("decode800_ctx500", [(500, 1)] * 800)
         attn_case("decode64_ctx2000", [(2000, 1)] * 64)
         attn_case("decode8_ctx8000", [(8000, 1)] * 8)
+        attn_case("decode800_ctx500_mixedkernel", [(500, 1)] * 800, force_mixed=True)
+        attn_case("bench_like_mix", [(500, 1)] * 800 + [(0, 300)] * 4 + [(150, 300)] * 1 + [(0, 50)] * 2)
         attn_case("prefill_4x300_from0", [(0, 300)] * 4)
         attn_case("prefill_chunk512_after1500", [(1500, 512)])
         attn_case("mixed_bench", [(500, 1)] * 800 + [(0, 300)] * 3 + [(200, 300)] * 1)
