@@ -98,7 +98,8 @@ typedef struct gllm_stage {
 } gllm_stage;
 
 /* One micro-batch. `meta` is ONE device int32 buffer holding, back to back:
- *   seq_info [n_seqs][5] | attention work [n_work][2] = (seq, q_start)
+ *   seq_info [n_seqs][5] | attention work [n_work][2] = (seq, q_start), the n_prefill_work
+ *     prefill tiles (gllm_attention_q_tile tokens each) FIRST, then one item per decode
  *   | page deltas [n_deltas][3] = (row, page_index, page_id)
  *   | prompt headers [n_prompts][3] = (row, length, token offset) | prompt tokens */
 typedef struct gllm_batch {

@@ -123,12 +123,15 @@ def test_attention_mixed(lib, n_heads, n_kv):
     info, work, off = [], [], 0
     for i, (s, n) in enumerate(seqs):
         info.append([i, s, n, off, -1])
-        work += [[i, q0] for q0 in range(0, n, q_tile)]
+        if n > 1:
+            work += [[i, q0] for q0 in range(0, n, q_tile)]
         off += n
+    n_pf = len(work)
+    work += [[i, 0] for i, (s, n) in enumerate(seqs) if n == 1]   # contract: prefill tiles first
     info_t = torch.tensor(info, dtype=torch.int32, device="cuda")
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
     out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
-    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), sum(1 for i, _ in work if seqs[i][1] > 1), table.data_ptr(),
+    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), n_pf, table.data_ptr(),
              mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
     torch.cuda.synchronize()
     g = n_heads // n_kv
