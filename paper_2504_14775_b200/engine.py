@@ -159,16 +159,37 @@ class SeqMeta:
 
 @dataclass
 class BatchMeta:
-    """Everything a stage worker needs for one micro-batch (the paper's pre-broadcast metadata)."""
+    """Everything a stage worker needs for one micro-batch (the paper's pre-broadcast metadata).
+
+    Columnar (one list per field, plan order) so packing is vectorised; `seqs`
+    materialises per-sequence `SeqMeta` views when a caller wants them.
+    """
 
     seq: int
-    seqs: list[SeqMeta]
+    ids: list[int]
+    rows: list[int]
+    starts: list[int]
+    n_new: list[int]
+    emits: list[bool]
     page_deltas: object                   # int32 [n, 3] (row, page_index, page_id)
     new_prompts: list[tuple[int, int]] = field(default_factory=list)  # (request_id, row)
 
+    @classmethod
+    def from_seqs(cls, seq: int, seqs: list[SeqMeta], page_deltas, new_prompts=()) -> "BatchMeta":
+        return cls(seq, [s.request_id for s in seqs], [s.row for s in seqs], [s.start for s in seqs],
+                   [s.n_new for s in seqs], [bool(s.emits) for s in seqs], page_deltas, list(new_prompts))
+
+    @property
+    def seqs(self) -> list[SeqMeta]:
+        return [SeqMeta(*t) for t in zip(self.ids, self.rows, self.starts, self.n_new, self.emits)]
+
     @property
     def n_tokens(self) -> int:
-        return sum(s.n_new for s in self.seqs)
+        return sum(self.n_new)
+
+    @property
+    def n_emit(self) -> int:
+        return sum(self.emits)
 
 
 @dataclass
@@ -313,15 +334,21 @@ class EngineCore:
         if self.executor is not None:
             self.executor.retire(batch.seq)
         self.committed_tokens += plan.total_tokens
+        back: list = []
+        reqs = self._reqs
         for rid in plan.decode_ids:
-            r = self._reqs[rid]
+            r = reqs[rid]
             r.in_flight = False
             r.generated += 1
             r.incarnation += 1
             if r.generated >= r.spec.output_tokens:
                 self._finish(r, t)
             else:
-                insort(self._ready, r.key)
+                back.append(r.key)
+        if back:
+            # re-queue in one merge (timsort on two sorted runs) instead of an insort per decode
+            self._ready.extend(back)
+            self._ready.sort()
         for rid, n in plan.prefill_chunks:
             r = self._reqs[rid]
             r.in_flight = False
@@ -355,7 +382,8 @@ class EngineCore:
         else:
             chosen = [k[1] for k in self._ready]
             limit = min(max(0, self._token_budget - len(chosen)), self._wp)
-        stored = [kv.stored_tokens(rid) for rid in chosen]
+        toks = kv._tokens
+        stored = [toks[rid] for rid in chosen]   # decode-ready requests always hold KV
         reserved = sum(1 for s in stored if s % ps == 0)
 
         def cands():
@@ -385,6 +413,17 @@ class EngineCore:
         kv = self.kv
         paged = isinstance(kv, PagedKvCache)
         mutated = False
+        # Fast path: a decode needs a page only when its stored length is a page multiple;
+        # if every such page is free, sequential allocate(rid, 1) would succeed for all of
+        # them with no eviction, so apply them in bulk (same state, same delta order).
+        if plan.decode_ids and kv.bulk_append_one(plan.decode_ids):
+            plan.decode_context_tokens = kv.last_bulk_context
+            for rid, n in plan.prefill_chunks:
+                if paged:
+                    self._bind_row(rid)
+                if not kv.allocate(rid, n):
+                    raise AssertionError("prefill pages were reserved at planning time")
+            return False
         kept: list[int] = []
         dropped: set[int] = set()
         for rid in plan.decode_ids:
@@ -434,26 +473,31 @@ class EngineCore:
         batch = _Batch(seq, plan, stage_time(plan, self._pipeline.cost),
                        transfer_time(plan, self._pipeline.comm))
         reqs = self._reqs
-        metas: list[SeqMeta] | None = [] if self.executor is not None else None
-        for rid in plan.decode_ids:
-            r = reqs[rid]
+        dec = plan.decode_ids
+        dec_reqs = [reqs[rid] for rid in dec]
+        for r in dec_reqs:
             r.in_flight = True
-            if metas is not None:
-                # stored_tokens already counts the token being appended now.
-                metas.append(SeqMeta(rid, r.row, self.kv.stored_tokens(rid) - 1, 1, True))
         for rid, n in plan.prefill_chunks:
             r = reqs[rid]
             r.in_flight = True
             r.inflight = n
             self._wp -= n
-            if metas is not None:
-                metas.append(SeqMeta(rid, r.row, r.done, n,
-                                     r.done + n >= r.target and r.generated == 0))
-        _remove_prefix_ids(self._ready, plan.decode_ids, reqs)
-        _remove_prefix_ids(self._waiting, [rid for rid, _ in plan.prefill_chunks], reqs)
-        if metas is not None:
-            batch.meta = BatchMeta(seq, metas, self.kv.take_deltas(), self._pending_prompts)
+        if self.executor is not None:
+            toks = self.kv._tokens
+            chunks = plan.prefill_chunks
+            ch_reqs = [reqs[rid] for rid, _ in chunks]
+            batch.meta = BatchMeta(
+                seq,
+                dec + [rid for rid, _ in chunks],
+                [r.row for r in dec_reqs] + [r.row for r in ch_reqs],
+                # stored_tokens already counts the token a decode appends now
+                [toks[rid] - 1 for rid in dec] + [r.done for r in ch_reqs],
+                [1] * len(dec) + [n for _, n in chunks],
+                [True] * len(dec) + [r.done + n >= r.target and r.generated == 0 for r, (_, n) in zip(ch_reqs, chunks)],
+                self.kv.take_deltas(), self._pending_prompts)
             self._pending_prompts = []
+        _remove_prefix_ids(self._ready, dec, reqs)
+        _remove_prefix_ids(self._waiting, [rid for rid, _ in plan.prefill_chunks], reqs)
         self.in_flight[seq] = batch
         self._iters.append(IterationRecord(seq, t, plan.prefill_tokens, plan.decode_tokens))
         return batch
@@ -491,7 +535,7 @@ def _remove_prefix_ids(keys: list, ids: list[int], reqs: dict) -> None:
     if not ids:
         return
     n = len(ids)
-    if n <= len(keys) and all(keys[i][1] == ids[i] for i in range(n)):
+    if n <= len(keys) and [k[1] for k in keys[:n]] == ids:
         del keys[:n]
         return
     for rid in ids:

@@ -102,6 +102,32 @@ class KvCacheState:
         self._revoke(request_id)
         return n
 
+    def bulk_append_one(self, request_ids) -> bool:
+        """Append one token to each request iff that needs no more pages than are free.
+
+        Equivalent to calling `allocate(rid, 1)` in order when every call would
+        succeed (each needs 0 or 1 page, so that holds exactly when the total fits);
+        returns False and changes nothing otherwise. Sets `last_bulk_context` to
+        the sum of the new stored lengths (the plan's decode context).
+        """
+        ps = self.config.page_size
+        toks = self._tokens
+        crossing = [rid for rid in request_ids if toks[rid] % ps == 0]
+        if len(crossing) > self.free_pages:
+            return False
+        ctx = 0
+        for rid in request_ids:
+            v = toks[rid] + 1
+            toks[rid] = v
+            ctx += v
+        pages = self._pages
+        for rid in crossing:
+            pages[rid] += 1
+            self._grant(rid, 1)
+        self.free_pages -= len(crossing)
+        self.last_bulk_context = ctx
+        return True
+
     # hooks for the physical layer
     def _grant(self, request_id: int, n_pages: int) -> None:
         pass

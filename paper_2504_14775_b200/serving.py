@@ -91,7 +91,7 @@ class ServingEngine(EngineCore):
                 self.clock = t
                 self.makespan_ms = max(self.makespan_ms, t)
                 batch = self.in_flight[seq]
-                n_out = sum(1 for s in batch.meta.seqs if s.emits)
+                n_out = batch.meta.n_emit
                 self._commit(t, batch)
                 self.commit_log.append((seq, t, n_out))
                 commits += 1

@@ -42,33 +42,35 @@ class PackedBatch:
 
 
 def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
-    """Pack `engine.BatchMeta` into the device metadata layout.
+    """Pack `engine.BatchMeta` into the device metadata layout (vectorised over sequences).
 
     `prompt_source(request_id) -> np.int32 array` supplies prompt tokens of
     requests that got a block-table row in this batch.
     """
-    seqs = meta.seqs
-    n = len(seqs)
-    info = np.empty((n, native.SEQ_FIELDS), dtype=np.int32)
-    emit_ids, emit_pos = [], []
-    off = 0
-    work_pf, work_dec = [], []
-    for i, s in enumerate(seqs):
-        e = -1
-        if s.emits:
-            e = len(emit_ids)
-            emit_ids.append(s.request_id)
-            emit_pos.append(s.start + s.n_new)
-        info[i] = (s.row, s.start, s.n_new, off, e)
-        off += s.n_new
-        if s.n_new == 1:
-            work_dec.append((i, 0))
-        else:
-            work_pf.extend((i, q0) for q0 in range(0, s.n_new, q_tile))
-    # Heavy prefill tiles first: CTAs launch in work order, so they overlap the decode stream
-    # instead of forming the tail of the launch.
-    n_prefill_work = len(work_pf)
-    work_a = np.asarray(work_pf + work_dec, dtype=np.int32).reshape(-1, 2)
+    n = len(meta.ids)
+    n_new = np.asarray(meta.n_new, dtype=np.int32).reshape(-1)
+    starts = np.asarray(meta.starts, dtype=np.int32).reshape(-1)
+    emits = np.asarray(meta.emits, dtype=bool).reshape(-1)
+    off = np.zeros(n, dtype=np.int32)
+    if n:
+        np.cumsum(n_new[:-1], out=off[1:])
+    emit_idx = np.where(emits, np.cumsum(emits) - 1, -1).astype(np.int32)
+    info = np.stack([np.asarray(meta.rows, dtype=np.int32).reshape(-1), starts, n_new, off, emit_idx], axis=1)
+    eidx = np.flatnonzero(emits)
+    emit_ids = [meta.ids[i] for i in eidx.tolist()]
+    emit_pos = (starts[eidx] + n_new[eidx]).tolist()
+    # attention work: prefill tiles first (heavy CTAs launch first), then one item per decode
+    pf = np.flatnonzero(n_new > 1)
+    tiles = (n_new[pf] + q_tile - 1) // q_tile
+    total = int(tiles.sum())
+    first = np.zeros(len(pf), dtype=np.int64)
+    if len(pf):
+        np.cumsum(tiles[:-1], out=first[1:])
+    pf_seq = np.repeat(pf, tiles)
+    pf_q0 = (np.arange(total) - np.repeat(first, tiles)) * q_tile
+    dec = np.flatnonzero(n_new == 1)
+    work_a = np.concatenate([np.stack([pf_seq, pf_q0], axis=1).reshape(-1, 2),
+                             np.stack([dec, np.zeros_like(dec)], axis=1).reshape(-1, 2)]).astype(np.int32)
     deltas = np.asarray(meta.page_deltas, dtype=np.int32).reshape(-1, 3)
     hdrs, toks = [], []
     toff = 0
@@ -78,10 +80,9 @@ def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
         toks.append(t)
         toff += len(t)
     hdr_a = np.asarray(hdrs, dtype=np.int32).reshape(-1, 3)
-    parts = [info.ravel(), work_a.ravel(), deltas.ravel(), hdr_a.ravel()] + toks
-    data = np.concatenate(parts) if parts else np.zeros(0, np.int32)
-    return PackedBatch(meta.seq, n, off, len(emit_ids), len(work_a), n_prefill_work, len(deltas), len(hdrs),
-                       data.astype(np.int32, copy=False), emit_ids, emit_pos)
+    data = np.concatenate([info.ravel(), work_a.ravel(), deltas.ravel(), hdr_a.ravel()] + toks).astype(np.int32)
+    return PackedBatch(meta.seq, n, int(n_new.sum()), len(emit_ids), len(work_a), total, len(deltas), len(hdrs),
+                       data, emit_ids, emit_pos)
 
 
 class StageWorker:

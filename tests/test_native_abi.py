@@ -54,8 +54,8 @@ def test_pack_batch_layout():
 
     from paper_2504_14775_b200.engine import BatchMeta, SeqMeta
     from paper_2504_14775_b200.stage import pack_batch
-    meta = BatchMeta(seq=3, seqs=[SeqMeta(7, 2, 40, 1, True), SeqMeta(9, 5, 0, 70, False), SeqMeta(4, 1, 10, 5, True)],
-                     page_deltas=np.array([[5, 0, 11], [5, 1, 12]], np.int32), new_prompts=[(9, 5)])
+    meta = BatchMeta.from_seqs(3, [SeqMeta(7, 2, 40, 1, True), SeqMeta(9, 5, 0, 70, False), SeqMeta(4, 1, 10, 5, True)],
+                               np.array([[5, 0, 11], [5, 1, 12]], np.int32), [(9, 5)])
     pb = pack_batch(meta, 32, lambda rid: np.arange(3, dtype=np.int32) + 100)
     assert (pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_prefill_work, pb.n_deltas, pb.n_prompts) == (3, 76, 2, 5, 4, 2, 1)
     d = pb.data
