@@ -76,7 +76,9 @@ typedef struct gllm_layer {
   const void* b_qkv;      /* bf16 [(n_heads + 2 n_kv) * hd] or NULL */
   const void* w_o;        /* bf16 [d, n_heads * hd] */
   const void* mlp_norm;   /* bf16 [d] */
-  const void* w_gate_up;  /* bf16 [2 d_ff, d]: gate rows then up rows */
+  const void* w_gate_up;  /* bf16 [2 d_ff, d]: 64-row blocks alternating gate / up (rows 128j..128j+63 =
+                             gate rows 64j.., rows 128j+64.. = up rows 64j..), so a GEMM tile holds
+                             matching gate/up outputs and SiLU*mul runs in its epilogue */
   const void* w_down;     /* bf16 [d, d_ff] */
 } gllm_layer;
 
@@ -143,6 +145,10 @@ GLLM_API int gllm_commit_tokens(const gllm_stage* stage, const gllm_batch* batch
 GLLM_API int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N, int K,
                    const void* bias, const void* residual, int ldr, int force_bn, int force_splits,
                    void* workspace, size_t workspace_bytes, gllm_stream_t stream);
+/* act[M, d_ff] = silu(A . W_gate^T) * (A . W_up^T), W in the interleaved w_gate_up layout above */
+GLLM_API int gllm_gemm_swiglu_bf16(const void* A, int lda, const void* B_interleaved, int ldb, void* act, int ldc,
+                                   int M, int d_ff, int K, int force_bn, int force_splits, void* workspace,
+                                   size_t workspace_bytes, gllm_stream_t stream);
 GLLM_API int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,
                  float eps, gllm_stream_t stream);
 GLLM_API int gllm_silu_mul(const void* gate_up, int d_ff, void* out, int rows, gllm_stream_t stream);

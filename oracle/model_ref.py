@@ -90,6 +90,6 @@ class RefDecoder:
 def from_stage_workers(workers) -> RefDecoder:
     """Oracle over the same bf16 weights the GPU stage workers hold (read back once)."""
     spec = workers[0].spec
-    layers = [L for w in workers for L in w.layers]
+    layers = [L for w in workers for L in w.canonical_layers()]
     first, last = workers[0], workers[-1]
     return RefDecoder(spec, layers, first.rope.cpu().numpy(), first.embed, last.final_norm, last.lm_head)

@@ -31,7 +31,7 @@ struct GemmSmem {
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
 };
 
-enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1 };
+enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1, EPI_SWIGLU = 2 };
 
 template <int BN, int STAGES, int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -117,6 +117,37 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
     const int row = m0 + q * 32 + lane;
     mbar_wait(tmem_full, 0);
     tc_fence_after();
+    if constexpr (MODE == EPI_SWIGLU) {
+      // B rows interleave 64 gate / 64 up rows, so TMEM columns [128p, 128p+64) are gate
+      // and [128p+64, 128p+128) the matching up outputs of this thread's token row:
+      // act = bf16(silu(bf16 g)) * bf16(u), the same roundings as a separate SiLU kernel.
+#pragma unroll 1
+      for (int p = 0; p < BN / 128; ++p) {
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 32) {
+          uint32_t g[32], u[32];
+          const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+          tmem_ld_32x32b_x32(lane_base + (uint32_t)(128 * p + c), g);
+          tmem_ld_32x32b_x32(lane_base + (uint32_t)(128 * p + 64 + c), u);
+          tmem_ld_wait();
+          const int ocol = (n0 >> 1) + 64 * p + c;
+          if (row >= M || ocol >= (N >> 1)) continue;
+          uint32_t packed[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float a0 = bf2f(f2bf(__uint_as_float(g[2 * j]))), a1 = bf2f(f2bf(__uint_as_float(g[2 * j + 1])));
+            const float b0 = bf2f(f2bf(__uint_as_float(u[2 * j]))), b1 = bf2f(f2bf(__uint_as_float(u[2 * j + 1])));
+            a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
+            a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
+            packed[j] = pack_bf16x2(a0 * b0, a1 * b1);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ldc + ocol);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+        }
+      }
+    } else
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
@@ -217,6 +248,38 @@ __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int
       make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
 }
 
+// Split-K reduce for the SwiGLU GEMM: N = 2*d_ff interleaved columns -> act[M, d_ff].
+// Output column o reads gate column 128*(o/64) + o%64 and up column gate + 64.
+__global__ void splitk_reduce_swiglu(const float* __restrict__ partial, int splits, int M, int N,
+                                     bf16* __restrict__ C, int ldc) {
+  const int half = N / 2;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)M * (half / 8)) return;
+  const int row = (int)(idx / (half / 8));
+  const int o = (int)(idx % (half / 8)) * 8;
+  const int gcol = 128 * (o / 64) + o % 64;
+  float g[8], u[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) g[j] = u[j] = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float* base = partial + ((size_t)s * M + row) * N;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      g[j] += base[gcol + j];
+      u[j] += base[gcol + 64 + j];
+    }
+  }
+  uint32_t pk[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float a0 = bf2f(f2bf(g[2 * j])), a1 = bf2f(f2bf(g[2 * j + 1]));
+    a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
+    a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
+    pk[j] = pack_bf16x2(a0 * bf2f(f2bf(u[2 * j])), a1 * bf2f(f2bf(u[2 * j + 1])));
+  }
+  *reinterpret_cast<uint4*>(C + (size_t)row * ldc + o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+}
+
 // ------------------------------------------------------------------ host side
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -306,21 +369,26 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   return check_launch("gemm_bf16_tcgen05");
 }
 
-int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
-              const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits,
-              void* workspace, size_t ws_bytes, cudaStream_t st) {
+// swiglu != 0: B is the 64-row-interleaved [gate|up] weight (N = 2*d_ff) and C receives
+// act = silu(gate) * up as [M, N/2]; tiles must cover whole 128-row gate/up pairs (BN >= 128).
+static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
+                     const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn,
+                     int force_splits, int swiglu, void* workspace, size_t ws_bytes, cudaStream_t st) {
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return set_error(GLLM_ERR_INVALID, "gemm needs K %% 64 == 0 and N %% 64 == 0 (K=%d N=%d)", K, N);
   if (ldc % 8 || (residual && ldr % 8)) return set_error(GLLM_ERR_INVALID, "gemm output pitch must be a multiple of 8");
+  if (swiglu && (N % 128 || bias || residual)) return set_error(GLLM_ERR_INVALID, "swiglu gemm needs N %% 128 == 0, no bias/residual");
   const int num_sms = device_sm_count();
   const int m_tiles = (M + BM - 1) / BM;
+  const int min_bn = swiglu ? 128 : 64;
   // Tile width: widest that still yields at least one wave of CTAs.
   int bn = force_bn;
   if (bn == 0) {
     bn = 256;
-    while (bn > 64 && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
+    while (bn > min_bn && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
     if (N % bn) bn = (N % 128 == 0) ? 128 : 64;
   }
+  if (swiglu && bn < 128) return set_error(GLLM_ERR_INVALID, "swiglu gemm needs BN >= 128");
   const int n_tiles = N / bn;
   const int total_kb = K / BK;
   int splits = force_splits;
@@ -346,26 +414,57 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, 
   if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;
   if (int rc = make_map(&mb, B, N, K, ldb, bn)) return rc;
   int rc = 0;
-  const int mode = splits > 1 ? EPI_PARTIAL_F32 : EPI_STORE;
+  const int mode = splits > 1 ? EPI_PARTIAL_F32 : (swiglu ? EPI_SWIGLU : EPI_STORE);
 #define GLLM_GEMM_CASE(BNV, ST)                                                                              \
   if (bn == BNV) {                                                                                           \
-    rc = mode == EPI_STORE ? launch_gemm<BNV, ST, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias,    \
-                                                             residual, ldr, nullptr, st)                     \
-                           : launch_gemm<BNV, ST, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc,    \
-                                                                   nullptr, nullptr, 0, partial, st);        \
+    if (mode == EPI_STORE)                                                                                   \
+      rc = launch_gemm<BNV, ST, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual, ldr,       \
+                                           nullptr, st);                                                     \
+    else if (mode == EPI_PARTIAL_F32)                                                                        \
+      rc = launch_gemm<BNV, ST, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0, \
+                                                 partial, st);                                               \
+    else                                                                                                     \
+      rc = launch_gemm<BNV, ST, EPI_SWIGLU>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0,      \
+                                            nullptr, st);                                                    \
   }
   GLLM_GEMM_CASE(256, 4)
-  else GLLM_GEMM_CASE(128, 6) else GLLM_GEMM_CASE(64, 8) else return set_error(GLLM_ERR_INVALID, "bad BN %d", bn);
+  else GLLM_GEMM_CASE(128, 6) else if (bn == 64 && !swiglu) {
+    rc = mode == EPI_STORE ? launch_gemm<64, 8, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual,
+                                                           ldr, nullptr, st)
+                           : launch_gemm<64, 8, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr,
+                                                                 nullptr, 0, partial, st);
+  } else return set_error(GLLM_ERR_INVALID, "bad BN %d", bn);
 #undef GLLM_GEMM_CASE
   if (rc) return rc;
   if (splits > 1) {
-    const size_t groups = (size_t)M * (N / 8);
     const int threads = 256;
-    splitk_reduce<<<(unsigned)((groups + threads - 1) / threads), threads, 0, st>>>(partial, splits, M, N, C, ldc,
-                                                                                   bias, residual, ldr);
-    rc = check_launch("splitk_reduce");
+    if (swiglu) {
+      const size_t groups = (size_t)M * (N / 2 / 8);
+      splitk_reduce_swiglu<<<(unsigned)((groups + threads - 1) / threads), threads, 0, st>>>(partial, splits, M, N,
+                                                                                             C, ldc);
+      rc = check_launch("splitk_reduce_swiglu");
+    } else {
+      const size_t groups = (size_t)M * (N / 8);
+      splitk_reduce<<<(unsigned)((groups + threads - 1) / threads), threads, 0, st>>>(partial, splits, M, N, C, ldc,
+                                                                                     bias, residual, ldr);
+      rc = check_launch("splitk_reduce");
+    }
   }
   return rc;
+}
+
+int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
+              const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits,
+              void* workspace, size_t ws_bytes, cudaStream_t st) {
+  return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, bias, residual, ldr, a_rows_alloc, force_bn, force_splits, 0,
+                   workspace, ws_bytes, st);
+}
+
+int gemm_swiglu_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int d_ff, int K,
+                     int a_rows_alloc, int force_bn, int force_splits, void* workspace, size_t ws_bytes,
+                     cudaStream_t st) {
+  return gemm_impl(A, lda, B, ldb, C, ldc, M, 2 * d_ff, K, nullptr, nullptr, 0, a_rows_alloc, force_bn, force_splits,
+                   1, workspace, ws_bytes, st);
 }
 
 size_t gemm_workspace_bytes(int M, int N, int K) {

@@ -21,6 +21,10 @@ int device_sm_count();
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K, const bf16* bias,
               const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits, void* workspace,
               size_t ws_bytes, cudaStream_t st);
+// act[M, d_ff] = silu(A W_g^T) * (A W_u^T) with W = the 64-row-interleaved [gate|up] weight [2 d_ff, K]
+int gemm_swiglu_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int d_ff, int K,
+                     int a_rows_alloc, int force_bn, int force_splits, void* workspace, size_t ws_bytes,
+                     cudaStream_t st);
 size_t gemm_workspace_bytes(int M, int N, int K);
 // bf16 [rows, cols] (leading dim ld) as a TMA map with 64-col x box_rows boxes, 128B swizzle (cached)
 int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);

@@ -4,7 +4,7 @@
 // one host call (no per-kernel Python round trips): metadata apply + device
 // slot mapping, embedding (first stage), then per layer
 //   RMSNorm -> QKV GEMM(+bias) -> RoPE + paged KV write -> mixed paged attention
-//   -> O GEMM(+residual) -> RMSNorm -> gate-up GEMM -> SiLU*mul -> down GEMM(+residual)
+//   -> O GEMM(+residual) -> RMSNorm -> gate-up GEMM with fused SiLU*mul -> down GEMM(+residual)
 // and on the last stage final RMSNorm of the emitting rows -> LM head GEMM -> argmax.
 // This is the real work behind the reference's `stage_time()` stand-in
 // (`pkg/src/tokensim/engine.py:96-100`).
@@ -271,13 +271,14 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
     if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
                         [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st); })))
       return rc;
-    if ((rc = prof_call(P_GEMM_GU, 2.0 * Td * 2 * Fd * Dd, gemm_bytes(Td, 2 * Fd, Dd, false, false), st, [&] {
-           return gemm_bf16(w.h, D, (const bf16*)L.w_gate_up, D, w.gu, 2 * d.d_ff, T, 2 * d.d_ff, D, nullptr, nullptr,
-                            0, maxT, 0, 0, w.gemm, w.gemm_bytes, st);
+    // gate-up GEMM with SiLU*mul fused into its epilogue: writes act [T, d_ff] directly
+    if ((rc = prof_call(P_GEMM_GU, 2.0 * Td * 2 * Fd * Dd,
+                        2.0 * (Td * Dd + 2 * Fd * Dd + Td * Fd), st, [&] {
+           return gemm_swiglu_bf16(w.h, D, (const bf16*)L.w_gate_up, D, w.act, d.d_ff, T, d.d_ff, D, maxT, 0, 0,
+                                   w.gemm, w.gemm_bytes, st);
          })))
       return rc;
-    GLLM_CHECK(w.gu, (size_t)T * 2 * d.d_ff, "gemm_gate_up", l);
-    if ((rc = prof_call(P_SILU, 0, 6.0 * Td * Fd, st, [&] { return silu_mul(w.gu, d.d_ff, w.act, T, st); }))) return rc;
+    GLLM_CHECK(w.act, (size_t)T * d.d_ff, "gemm_gate_up_swiglu", l);
     if ((rc = prof_call(P_GEMM_DOWN, 2.0 * Td * Dd * Fd, gemm_bytes(Td, Dd, Fd, true, false), st, [&] {
            return gemm_bf16(w.act, d.d_ff, (const bf16*)L.w_down, d.d_ff, x, D, T, D, d.d_ff, nullptr, x, D, maxT, 0,
                             0, w.gemm, w.gemm_bytes, st);
@@ -341,6 +342,13 @@ int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int 
   return gemm_bf16((const bf16*)A, lda, (const bf16*)B, ldb, (bf16*)C, ldc, M, N, K, (const bf16*)bias,
                    (const bf16*)residual, ldr, M, force_bn, force_splits, workspace, workspace_bytes,
                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_gemm_swiglu_bf16(const void* A, int lda, const void* B_interleaved, int ldb, void* act, int ldc, int M,
+                          int d_ff, int K, int force_bn, int force_splits, void* workspace, size_t workspace_bytes,
+                          gllm_stream_t stream) {
+  return gemm_swiglu_bf16((const bf16*)A, lda, (const bf16*)B_interleaved, ldb, (bf16*)act, ldc, M, d_ff, K, M,
+                          force_bn, force_splits, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,

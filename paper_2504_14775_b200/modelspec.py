@@ -135,6 +135,18 @@ def init_layer(spec: ModelSpec, layer: int, seed: int, device) -> dict:
     return out
 
 
+def interleave_gate_up(w, d_ff: int, block: int = 64):
+    """[gate; up] ([2 d_ff, d]) -> 64-row alternating gate/up blocks (the fused-SwiGLU GEMM layout)."""
+    d = w.shape[-1]
+    return w.view(2, d_ff // block, block, d).transpose(0, 1).reshape(2 * d_ff, d)
+
+
+def deinterleave_gate_up(w, d_ff: int, block: int = 64):
+    """Inverse of `interleave_gate_up`."""
+    d = w.shape[-1]
+    return w.view(d_ff // block, 2, block, d).transpose(0, 1).reshape(2 * d_ff, d)
+
+
 def init_embed(spec: ModelSpec, seed: int, device, which: str):
     """`embed` ([vocab, d]), `lm_head` ([vocab, d]) or `final_norm` ([d])."""
     import torch

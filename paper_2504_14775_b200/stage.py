@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import native
-from .modelspec import ModelSpec, init_embed, init_layer, rope_table
+from .modelspec import ModelSpec, deinterleave_gate_up, init_embed, init_layer, interleave_gate_up, rope_table
 from .workload import prompt_token_ids
 
 
@@ -107,6 +107,8 @@ class StageWorker:
         self.q_tile = lib.gllm_attention_q_tile(spec.n_heads, spec.n_kv_heads)
         dev = self.device
         self.layers = [init_layer(spec, l, seed, dev) for l in self.layer_ids]
+        for w in self.layers:   # device layout for the fused SwiGLU epilogue (see include/gllm.h)
+            w["w_gate_up"] = interleave_gate_up(w["w_gate_up"], spec.d_ff).contiguous()
         self.embed = init_embed(spec, seed, dev, "embed") if is_first else None
         self.final_norm = init_embed(spec, seed, dev, "final_norm") if is_last else None
         self.lm_head = init_embed(spec, seed, dev, "lm_head") if is_last else None
@@ -131,6 +133,15 @@ class StageWorker:
                                    native.ptr(self.final_norm), native.ptr(self.lm_head), self._layer_arr,
                                    native.ptr(self.k_cache), native.ptr(self.v_cache), native.ptr(self.block_table),
                                    native.ptr(self.token_hist), native.ptr(self.rope), native.ptr(self.workspace), ws)
+
+    def canonical_layers(self) -> list[dict]:
+        """Layer weights in the plain [gate; up] layout (for the fp32 oracle)."""
+        out = []
+        for w in self.layers:
+            c = dict(w)
+            c["w_gate_up"] = deinterleave_gate_up(w["w_gate_up"], self.spec.d_ff)
+            out.append(c)
+        return out
 
     def cbatch(self, pb: PackedBatch, meta_dev, hidden=None, sampled=None, logits=None) -> native.Batch:
         # host seq_info view for the profiler's byte/FLOP accounting (first n_seqs*5 ints)

@@ -53,6 +53,25 @@ def test_gemm_tcgen05(lib, M, N, K):
     assert _rel(C_, ref + bias.float() + res.float()) < 8e-3
 
 
+@pytest.mark.parametrize("M,d_ff,K", [(1, 768, 256), (37, 14336, 4096), (300, 768, 256), (2048, 14336, 4096)])
+def test_gemm_swiglu_fused(lib, M, d_ff, K):
+    from paper_2504_14775_b200.modelspec import interleave_gate_up
+    g = torch.Generator(device="cuda").manual_seed(M + d_ff)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(2 * d_ff, K, device="cuda", generator=g) * 0.05).bfloat16()
+    Wi = interleave_gate_up(W, d_ff).contiguous()
+    ws = torch.empty(160 << 20, dtype=torch.uint8, device="cuda")
+    gu = (A.float() @ W.float().T).bfloat16().float()
+    ref = torch.nn.functional.silu(gu[:, :d_ff]).bfloat16().float() * gu[:, d_ff:]
+    for bn, splits in ((0, 0), (128, 1), (256, 1), (128, 3)):
+        act = torch.full((M, d_ff), float("nan"), device="cuda").bfloat16()
+        lib.call("gllm_gemm_swiglu_bf16", A.data_ptr(), K, Wi.data_ptr(), K, act.data_ptr(), d_ff, M, d_ff, K, bn,
+                 splits, ws.data_ptr(), ws.numel(), lib.stream_handle())
+        torch.cuda.synchronize()
+        assert torch.isfinite(act.float()).all(), (bn, splits)
+        assert _rel(act, ref) < 1e-2, (bn, splits, _rel(act, ref))
+
+
 def test_rmsnorm_and_silu(lib):
     x = torch.randn(37, 4096, device="cuda").bfloat16()
     w = (torch.rand(4096, device="cuda") + 0.5).bfloat16()
