@@ -4,10 +4,12 @@
 //
 // A = activations (tokens x K), B = weights (out_features x K); both K-major
 // row-major bf16, exactly how the stage stores them, so no transposes.
-// One CTA owns a 128 x BN output tile (optionally a K-slice of it, split-K):
+// Persistent (one CTA per SM) over 128 x BN output tiles (optionally K-slices, split-K):
 //   warp 0  : TMA producer (one elected lane), STAGES-deep smem ring
-//   warp 1  : TMEM allocator + MMA issuer (one lane), tcgen05.mma M=128,N=BN,K=16
-//   warps 2-5: epilogue, tcgen05.ld 32 lanes x 32 cols -> bf16 (+bias/+residual)
+//   warp 1  : TMEM allocator + MMA issuer (one lane), tcgen05.mma M=128,N=BN,K=16 into
+//             one of two TMEM accumulators (the epilogue drains the other)
+//   warps 2-5: epilogue, tcgen05.ld 32 lanes x 32 cols -> bf16 (+bias/+residual, or fused
+//             SiLU*mul for the interleaved gate-up weight)
 // Rows past M are zero-filled by TMA on load and masked on store, so decode
 // micro-batches (M = a few tokens) reuse the same kernel; they are HBM-bound on
 // the weight stream, and split-K spreads that stream over all 148 SMs.
@@ -28,139 +30,57 @@ struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers, TMEM slot*/;
 };
 
 enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1, EPI_SWIGLU = 2 };
 
-template <int BN, int STAGES, int MODE>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                  int M, int N, int K, int k_blocks_per_split, bf16* __restrict__ C, int ldc,
-                  const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
-                  float* __restrict__ partial) {
-  using L = GemmSmem<BN, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  // M-tiles vary fastest: the CTAs of one wave share each weight (B) tile through L2, so
-  // the weight matrix streams from HBM ~once per GEMM instead of once per M-tile.
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
-  const int total_kb = K / BK;
-  const int kb0 = blockIdx.z * k_blocks_per_split;
-  const int kb1 = min(total_kb, kb0 + k_blocks_per_split);
-  const int nkb = kb1 - kb0;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&map_a);
-    tma_prefetch_desc(&map_b);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tmem_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, BN);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();  // weights stream through once per step
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * L::STAGE_BYTES;
-        uint8_t* sb = sa + L::A_BYTES;
-        mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
-        const int kc = (kb0 + i) * BK;
-        tma_load_2d(&map_a, &full[s], sa, kc, m0);
-        tma_load_2d_hint(&map_b, &full[s], sb, kc, n0, pol_w);
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % STAGES;
-      const uint32_t ph = (i / STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint8_t* sa = smem + s * L::STAGE_BYTES;
-        const uint8_t* sb = sa + L::A_BYTES;
-        const uint64_t da = smem_desc_sw128(sa);
-        const uint64_t db = smem_desc_sw128(sb);
+// Epilogue of one 128 x BN output tile held in TMEM columns [acc_col, acc_col + BN):
+// warp (w % 4) reads TMEM lanes [32q, 32q+32), i.e. output rows m0 + 32q + lane.
+template <int BN, int MODE>
+__device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, int n0, int split, int M, int N,
+                                              bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
+                                              const bf16* __restrict__ residual, int ldr,
+                                              float* __restrict__ partial) {
+  if constexpr (MODE == EPI_SWIGLU) {
+    // B rows interleave 64 gate / 64 up rows, so TMEM columns [128p, 128p+64) are gate
+    // and [128p+64, 128p+128) the matching up outputs of this thread's token row:
+    // act = bf16(silu(bf16 g)) * bf16(u), the same roundings as a separate SiLU kernel.
+#pragma unroll 1
+    for (int p = 0; p < BN / 128; ++p) {
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t g[32], u[32];
+        tmem_ld_32x32b_x32(tmem_lane_base + (uint32_t)(128 * p + c), g);
+        tmem_ld_32x32b_x32(tmem_lane_base + (uint32_t)(128 * p + 64 + c), u);
+        tmem_ld_wait();
+        const int ocol = (n0 >> 1) + 64 * p + c;
+        if (row >= M || ocol >= (N >> 1)) continue;
+        uint32_t packed[16];
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          // +32 B along K inside the swizzle atom = +2 in the 16-byte address field.
-          mma_bf16_ss(tmem_base, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        for (int j = 0; j < 16; ++j) {
+          float a0 = bf2f(f2bf(__uint_as_float(g[2 * j]))), a1 = bf2f(f2bf(__uint_as_float(g[2 * j + 1])));
+          const float b0 = bf2f(f2bf(__uint_as_float(u[2 * j]))), b1 = bf2f(f2bf(__uint_as_float(u[2 * j + 1])));
+          a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
+          a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
+          packed[j] = pack_bf16x2(a0 * b0, a1 * b1);
         }
-        mma_commit(&empty[s]);
-        if (i == nkb - 1) mma_commit(tmem_full);
+        uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ldc + ocol);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
       }
-      __syncwarp();
     }
   } else {
-    // Epilogue: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    if constexpr (MODE == EPI_SWIGLU) {
-      // B rows interleave 64 gate / 64 up rows, so TMEM columns [128p, 128p+64) are gate
-      // and [128p+64, 128p+128) the matching up outputs of this thread's token row:
-      // act = bf16(silu(bf16 g)) * bf16(u), the same roundings as a separate SiLU kernel.
-#pragma unroll 1
-      for (int p = 0; p < BN / 128; ++p) {
-#pragma unroll 1
-        for (int c = 0; c < 64; c += 32) {
-          uint32_t g[32], u[32];
-          const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
-          tmem_ld_32x32b_x32(lane_base + (uint32_t)(128 * p + c), g);
-          tmem_ld_32x32b_x32(lane_base + (uint32_t)(128 * p + 64 + c), u);
-          tmem_ld_wait();
-          const int ocol = (n0 >> 1) + 64 * p + c;
-          if (row >= M || ocol >= (N >> 1)) continue;
-          uint32_t packed[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float a0 = bf2f(f2bf(__uint_as_float(g[2 * j]))), a1 = bf2f(f2bf(__uint_as_float(g[2 * j + 1])));
-            const float b0 = bf2f(f2bf(__uint_as_float(u[2 * j]))), b1 = bf2f(f2bf(__uint_as_float(u[2 * j + 1])));
-            a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
-            a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
-            packed[j] = pack_bf16x2(a0 * b0, a1 * b1);
-          }
-          uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ldc + ocol);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-        }
-      }
-    } else
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c, r);
+      tmem_ld_32x32b_x32(tmem_lane_base + (uint32_t)c, r);
       tmem_ld_wait();
       const int col = n0 + c;
       if (row >= M || col >= N) continue;
-      if (nkb <= 0) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = 0u;
-      }
       if constexpr (MODE == EPI_PARTIAL_F32) {
-        float4* dst = reinterpret_cast<float4*>(partial + ((size_t)blockIdx.z * M + row) * N + col);
+        float4* dst = reinterpret_cast<float4*>(partial + ((size_t)split * M + row) * N + col);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
@@ -200,9 +120,136 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
       }
     }
   }
+}
+
+// Persistent: one CTA per SM walks work units u = blockIdx.x, +gridDim.x, ... where a unit is
+// (m-tile, n-tile, K-split) with the m-tile fastest, so the CTAs running at the same time share
+// each weight (B) tile through L2 and the weight matrix streams from HBM ~once per GEMM.
+// The accumulator is double-buffered in TMEM (2 x BN columns): the epilogue of unit i overlaps
+// the MMAs of unit i+1; the smem ring's phases continue across units.
+template <int BN, int STAGES, int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                  int M, int N, int K, int k_blocks_per_split, int n_splits, bf16* __restrict__ C, int ldc,
+                  const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
+                  float* __restrict__ partial) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;    // [2] MMA -> epilogue
+  uint64_t* acc_empty = acc_full + 2;     // [2] epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_tiles = (M + BM - 1) / BM;
+  const int n_tiles = N / BN;
+  const int units = m_tiles * n_tiles * n_splits;
+  const int total_kb = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);   // one arrival per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, BN);
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto unit_coords = [&](int u, int& m0, int& n0, int& split, int& kb0, int& nkb) {
+    const int mt = u % m_tiles;
+    const int rest = u / m_tiles;
+    const int nt = rest % n_tiles;
+    split = rest / n_tiles;
+    m0 = mt * BM;
+    n0 = nt * BN;
+    kb0 = split * k_blocks_per_split;
+    nkb = min(total_kb, kb0 + k_blocks_per_split) - kb0;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();  // weights stream through once per step
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int m0, n0, split, kb0, nkb;
+        unit_coords(u, m0, n0, split, kb0, nkb);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * L::STAGE_BYTES;
+          uint8_t* sb = sa + L::A_BYTES;
+          mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+          const int kc = (kb0 + i) * BK;
+          tma_load_2d(&map_a, &full[s], sa, kc, m0);
+          tma_load_2d_hint(&map_b, &full[s], sb, kc, n0, pol_w);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+    int it = 0, lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      int m0, n0, split, kb0, nkb;
+      unit_coords(u, m0, n0, split, kb0, nkb);
+      const int acc = lt & 1;
+      mbar_wait(&acc_empty[acc], ((lt >> 1) & 1) ^ 1);   // epilogue drained this buffer
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint8_t* sa = smem + s * L::STAGE_BYTES;
+          const uint8_t* sb = sa + L::A_BYTES;
+          const uint64_t da = smem_desc_sw128(sa);
+          const uint64_t db = smem_desc_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 B along K inside the swizzle atom = +2 in the 16-byte address field.
+            mma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);
+          if (i == nkb - 1) mma_commit(&acc_full[acc]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // Epilogue warps 2-5: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+    const int q = warp & 3;
+    int lt = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+      int m0, n0, split, kb0, nkb;
+      unit_coords(u, m0, n0, split, kb0, nkb);
+      const int acc = lt & 1;
+      mbar_wait(&acc_full[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      epilogue_tile<BN, MODE>(lane_base, m0 + q * 32 + lane, n0, split, M, N, C, ldc, bias, residual, ldr, partial);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, 2 * BN);
 }
 
 // Sum split-K partials [splits, M, N] fp32 and apply the epilogue; 8 columns per thread.
@@ -363,9 +410,10 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_done = true;
   }
-  dim3 grid((M + BM - 1) / BM, N / BN, splits);
-  gemm_bf16_tcgen05<BN, STAGES, MODE><<<grid, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, C, ldc, bias, res,
-                                                                        ldr, partial);
+  const long units = (long)((M + BM - 1) / BM) * (N / BN) * splits;
+  const int grid = (int)(units < device_sm_count() ? units : device_sm_count());
+  gemm_bf16_tcgen05<BN, STAGES, MODE><<<grid, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, splits, C, ldc, bias,
+                                                                        res, ldr, partial);
   return check_launch("gemm_bf16_tcgen05");
 }
 
