@@ -130,8 +130,16 @@ def roofline(profile: dict, peaks: dict) -> dict:
         achieved = e["bytes"] / e["launches"] / (per_launch_ms * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
         out = {"bound": "hbm", "unit": "GB/s", "algorithmic_per_launch": e["bytes"] / e["launches"]}
+    traffic = None
+    try:  # DRAM bytes per launch of this kernel class from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as fh:
+            t = json.load(fh).get(name)
+        if t:
+            traffic = {"bytes_per_launch": t["dram_bytes_per_launch"], "shape": t["shape"]}
+    except OSError:
+        pass
     out.update({"kernel": name, "achieved": round(achieved, 2), "peak": peak, "frac": round(achieved / peak, 4),
-                "traffic": None, "launches": e["launches"], "avg_launch_ms": round(per_launch_ms, 4),
+                "traffic": traffic, "launches": e["launches"], "avg_launch_ms": round(per_launch_ms, 4),
                 "peak_src": peaks["src"] + (" sustained" if out["bound"] == "tensor" else "")})
     return out
 
@@ -186,6 +194,7 @@ def run_ours(args):
                 st["timed_start"] = time.perf_counter()
                 st["t_engine"] = t
                 st["launch0"] = native.launch_count()
+                torch.cuda.nvtx.range_push("bench_timed")   # ncu --nvtx --nvtx-include bench_timed/
                 clocks.start()
             return
         if st["phase"] == "timed":
@@ -194,6 +203,7 @@ def run_ours(args):
                 torch.cuda.synchronize()
                 st["timed_end"] = time.perf_counter()
                 st["launch1"] = native.launch_count()
+                torch.cuda.nvtx.range_pop()
                 st["clocks"] = clocks.stop()
                 st["phase"] = "profile"
                 if args.no_profile:

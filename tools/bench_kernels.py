@@ -71,14 +71,18 @@ def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False):
                       "hbm_frac": round(kv_bytes / ms / 1e6 / PEAK["hbm_gbs"], 3), "TFLOP/s": round(flops / ms / 1e9, 1)}))
 
 
-def gemm_case(M, N, K, bn=0, splits=0):
+def gemm_case(M, N, K, bn=0, splits=0, swiglu=False):
     A = torch.randn(M, K, device="cuda").bfloat16()
     B = torch.randn(N, K, device="cuda").bfloat16()
     C = torch.empty(M, N, device="cuda").bfloat16()
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     st = native.stream_handle()
-    fn = lambda: native.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, None, None, 0,
-                             bn, splits, ws.data_ptr(), ws.numel(), st)
+    if swiglu:
+        fn = lambda: native.call("gllm_gemm_swiglu_bf16", A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N // 2, M,
+                                 N // 2, K, bn, splits, ws.data_ptr(), ws.numel(), st)
+    else:
+        fn = lambda: native.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, None,
+                                 None, 0, bn, splits, ws.data_ptr(), ws.numel(), st)
     ms = timeit(fn)
     fl = 2 * M * N * K
     by = 2 * (M * K + N * K + M * N)
@@ -92,7 +96,13 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--case", default="")
+    ap.add_argument("--gemm", default="", help="M,N,K single GEMM case")
+    ap.add_argument("--swiglu", action="store_true")
     a = ap.parse_args()
+    if a.gemm:
+        M, N, K = (int(x) for x in a.gemm.split(","))
+        gemm_case(M, N, K, swiglu=a.swiglu)
+        raise SystemExit(0)
     if a.case:
         _orig = attn_case
         attn_case = lambda name, *x, **k: _orig(name, *x, **k) if name == a.case else None
