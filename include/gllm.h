@@ -149,6 +149,14 @@ GLLM_API int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void
 GLLM_API int gllm_gemm_swiglu_bf16(const void* A, int lda, const void* B_interleaved, int ldb, void* act, int ldc,
                                    int M, int d_ff, int K, int force_bn, int force_splits, void* workspace,
                                    size_t workspace_bytes, gllm_stream_t stream);
+/* QKV projection with RoPE + paged KV write fused into the GEMM epilogue: q heads of
+ * A . W^T (+bias) are rotated and written to qkv[M][(H+2KV)*128] (k/v columns untouched);
+ * k heads are rotated and k/v written to the paged cache slot tok_slot[row] of each token */
+GLLM_API int gllm_gemm_qkv_rope_bf16(const void* A, int lda, const void* W, int ldb, const void* bias, void* qkv,
+                                     int M, int K, int n_heads, int n_kv_heads, const int32_t* tok_pos,
+                                     const int32_t* tok_slot, const float* rope, void* k_cache, void* v_cache,
+                                     int page_size, int force_bn, int force_splits, void* workspace,
+                                     size_t workspace_bytes, gllm_stream_t stream);
 GLLM_API int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,
                  float eps, gllm_stream_t stream);
 GLLM_API int gllm_silu_mul(const void* gate_up, int d_ff, void* out, int rows, gllm_stream_t stream);

@@ -33,7 +33,17 @@ struct GemmSmem {
   static constexpr int TOTAL = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers, TMEM slot*/;
 };
 
-enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1, EPI_SWIGLU = 2 };
+enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3 };
+
+// Extra epilogue operands of EPI_QKV_ROPE (RoPE on q/k + paged KV-cache write).
+struct QkvRopeArgs {
+  const int* tok_pos;    // [M] absolute position of each token row
+  const int* tok_slot;   // [M] paged slot: page * page_size + offset
+  const float* rope;     // [max_pos][64][2] (cos, sin)
+  bf16* k_cache;         // this layer's [pages][n_kv][page_size][128]
+  bf16* v_cache;
+  int n_heads, n_kv, page_size;
+};
 
 // Epilogue of one 128 x BN output tile held in TMEM columns [acc_col, acc_col + BN):
 // warp (w % 4) reads TMEM lanes [32q, 32q+32), i.e. output rows m0 + 32q + lane.
@@ -41,8 +51,76 @@ template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, int n0, int split, int M, int N,
                                               bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
                                               const bf16* __restrict__ residual, int ldr,
-                                              float* __restrict__ partial) {
-  if constexpr (MODE == EPI_SWIGLU) {
+                                              float* __restrict__ partial, const QkvRopeArgs& qa) {
+  if constexpr (MODE == EPI_QKV_ROPE) {
+    // Head-aligned tile: columns [128h, 128h+128) are one whole head of this token row, so the
+    // rotate-half pairs (d, d+64) are thread-local. q heads are rotated and written back to C;
+    // k heads rotated and v heads copied straight into the paged cache slot of the token.
+    const bool live = row < M;
+    const int pos = live ? qa.tok_pos[row] : 0;
+    const int slot = live ? qa.tok_slot[row] : 0;
+    const int page = slot / qa.page_size, off = slot % qa.page_size;
+    const float2* cs = reinterpret_cast<const float2*>(qa.rope) + (size_t)pos * 64;
+#pragma unroll 1
+    for (int hl = 0; hl < BN / 128; ++hl) {
+      const int gh = (n0 >> 7) + hl;
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t x1[32], x2[32];
+        tmem_ld_32x32b_x32(tmem_lane_base + (uint32_t)(128 * hl + c), x1);
+        tmem_ld_32x32b_x32(tmem_lane_base + (uint32_t)(128 * hl + 64 + c), x2);
+        tmem_ld_wait();
+        if (!live) continue;
+        const int col1 = gh * 128 + c;
+        float a[32], b[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          a[j] = __uint_as_float(x1[j]);
+          b[j] = __uint_as_float(x2[j]);
+        }
+        if (bias != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            a[j] += bf2f(bias[col1 + j]);
+            b[j] += bf2f(bias[col1 + 64 + j]);
+          }
+        }
+        uint32_t y1[16], y2[16];
+        if (gh < qa.n_heads + qa.n_kv) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            // same roundings as GEMM -> bf16 -> RoPE kernel
+            const float p0 = bf2f(f2bf(a[j])), p1 = bf2f(f2bf(a[j + 1]));
+            const float q0 = bf2f(f2bf(b[j])), q1 = bf2f(f2bf(b[j + 1]));
+            const float2 c0 = cs[c + j], c1 = cs[c + j + 1];
+            y1[j / 2] = pack_bf16x2(p0 * c0.x - q0 * c0.y, p1 * c1.x - q1 * c1.y);
+            y2[j / 2] = pack_bf16x2(q0 * c0.x + p0 * c0.y, q1 * c1.x + p1 * c1.y);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            y1[j / 2] = pack_bf16x2(a[j], a[j + 1]);
+            y2[j / 2] = pack_bf16x2(b[j], b[j + 1]);
+          }
+        }
+        bf16* dst;
+        if (gh < qa.n_heads) {
+          dst = C + (size_t)row * ldc + gh * 128;
+        } else {
+          const int kvh = gh < qa.n_heads + qa.n_kv ? gh - qa.n_heads : gh - qa.n_heads - qa.n_kv;
+          bf16* cache = gh < qa.n_heads + qa.n_kv ? qa.k_cache : qa.v_cache;
+          dst = cache + (((size_t)page * qa.n_kv + kvh) * qa.page_size + off) * 128;
+        }
+        uint4* d1 = reinterpret_cast<uint4*>(dst + c);
+        uint4* d2 = reinterpret_cast<uint4*>(dst + 64 + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          d1[j] = make_uint4(y1[4 * j], y1[4 * j + 1], y1[4 * j + 2], y1[4 * j + 3]);
+          d2[j] = make_uint4(y2[4 * j], y2[4 * j + 1], y2[4 * j + 2], y2[4 * j + 3]);
+        }
+      }
+    }
+  } else if constexpr (MODE == EPI_SWIGLU) {
     // B rows interleave 64 gate / 64 up rows, so TMEM columns [128p, 128p+64) are gate
     // and [128p+64, 128p+128) the matching up outputs of this thread's token row:
     // act = bf16(silu(bf16 g)) * bf16(u), the same roundings as a separate SiLU kernel.
@@ -132,7 +210,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   int M, int N, int K, int k_blocks_per_split, int n_splits, bf16* __restrict__ C, int ldc,
                   const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
-                  float* __restrict__ partial) {
+                  float* __restrict__ partial, const QkvRopeArgs qa) {
   using L = GemmSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -241,7 +319,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
       mbar_wait(&acc_full[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      epilogue_tile<BN, MODE>(lane_base, m0 + q * 32 + lane, n0, split, M, N, C, ldc, bias, residual, ldr, partial);
+      epilogue_tile<BN, MODE>(lane_base, m0 + q * 32 + lane, n0, split, M, N, C, ldc, bias, residual, ldr, partial,
+                              qa);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
@@ -401,7 +480,7 @@ int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t col
 template <int BN, int STAGES, int MODE>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits, int kbps,
                        bf16* C, int ldc, const bf16* bias, const bf16* res, int ldr, float* partial,
-                       cudaStream_t st) {
+                       cudaStream_t st, const QkvRopeArgs& qa = QkvRopeArgs{}) {
   constexpr int smem = GemmSmem<BN, STAGES>::TOTAL;
   static bool attr_done = false;
   if (!attr_done) {
@@ -413,7 +492,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   const long units = (long)((M + BM - 1) / BM) * (N / BN) * splits;
   const int grid = (int)(units < device_sm_count() ? units : device_sm_count());
   gemm_bf16_tcgen05<BN, STAGES, MODE><<<grid, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, splits, C, ldc, bias,
-                                                                        res, ldr, partial);
+                                                                        res, ldr, partial, qa);
   return check_launch("gemm_bf16_tcgen05");
 }
 
@@ -421,14 +500,15 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
 // act = silu(gate) * up as [M, N/2]; tiles must cover whole 128-row gate/up pairs (BN >= 128).
 static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
                      const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn,
-                     int force_splits, int swiglu, void* workspace, size_t ws_bytes, cudaStream_t st) {
+                     int force_splits, int swiglu, void* workspace, size_t ws_bytes, cudaStream_t st,
+                     const QkvRopeArgs* qkv = nullptr) {
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return set_error(GLLM_ERR_INVALID, "gemm needs K %% 64 == 0 and N %% 64 == 0 (K=%d N=%d)", K, N);
   if (ldc % 8 || (residual && ldr % 8)) return set_error(GLLM_ERR_INVALID, "gemm output pitch must be a multiple of 8");
   if (swiglu && (N % 128 || bias || residual)) return set_error(GLLM_ERR_INVALID, "swiglu gemm needs N %% 128 == 0, no bias/residual");
   const int num_sms = device_sm_count();
   const int m_tiles = (M + BM - 1) / BM;
-  const int min_bn = swiglu ? 128 : 64;
+  const int min_bn = (swiglu || qkv) ? 128 : 64;
   // Tile width: widest that still yields at least one wave of CTAs.
   int bn = force_bn;
   if (bn == 0) {
@@ -436,7 +516,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     while (bn > min_bn && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
     if (N % bn) bn = (N % 128 == 0) ? 128 : 64;
   }
-  if (swiglu && bn < 128) return set_error(GLLM_ERR_INVALID, "swiglu gemm needs BN >= 128");
+  if ((swiglu || qkv) && bn < 128) return set_error(GLLM_ERR_INVALID, "swiglu/qkv gemm needs BN >= 128");
   const int n_tiles = N / bn;
   const int total_kb = K / BK;
   int splits = force_splits;
@@ -462,7 +542,15 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;
   if (int rc = make_map(&mb, B, N, K, ldb, bn)) return rc;
   int rc = 0;
-  const int mode = splits > 1 ? EPI_PARTIAL_F32 : (swiglu ? EPI_SWIGLU : EPI_STORE);
+  if (qkv && splits > 1) {
+    // small-M QKV: split-K plain GEMM, then the standalone RoPE + KV-write kernel
+    int rc = gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, bias, nullptr, 0, a_rows_alloc, force_bn, splits, 0,
+                       workspace, ws_bytes, st, nullptr);
+    if (rc) return rc;
+    return rope_kv_write(C, M, qkv->n_heads, qkv->n_kv, 128, qkv->tok_pos, qkv->tok_slot, qkv->rope, qkv->k_cache,
+                         qkv->v_cache, qkv->page_size, st);
+  }
+  const int mode = splits > 1 ? EPI_PARTIAL_F32 : (swiglu ? EPI_SWIGLU : (qkv ? EPI_QKV_ROPE : EPI_STORE));
 #define GLLM_GEMM_CASE(BNV, ST)                                                                              \
   if (bn == BNV) {                                                                                           \
     if (mode == EPI_STORE)                                                                                   \
@@ -471,17 +559,20 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     else if (mode == EPI_PARTIAL_F32)                                                                        \
       rc = launch_gemm<BNV, ST, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0, \
                                                  partial, st);                                               \
-    else                                                                                                     \
+    else if (mode == EPI_SWIGLU)                                                                             \
       rc = launch_gemm<BNV, ST, EPI_SWIGLU>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0,      \
                                             nullptr, st);                                                    \
+    else                                                                                                     \
+      rc = launch_gemm<BNV, ST, EPI_QKV_ROPE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, nullptr, 0,       \
+                                              nullptr, st, *qkv);                                            \
   }
   GLLM_GEMM_CASE(256, 4)
-  else GLLM_GEMM_CASE(128, 6) else if (bn == 64 && !swiglu) {
+  else GLLM_GEMM_CASE(128, 6) else if (bn == 64 && !swiglu && !qkv) {
     rc = mode == EPI_STORE ? launch_gemm<64, 8, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual,
                                                            ldr, nullptr, st)
                            : launch_gemm<64, 8, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr,
                                                                  nullptr, 0, partial, st);
-  } else return set_error(GLLM_ERR_INVALID, "bad BN %d", bn);
+  } else return set_error(GLLM_ERR_INVALID, "bad BN %d (swiglu/qkv need >= 128)", bn);
 #undef GLLM_GEMM_CASE
   if (rc) return rc;
   if (splits > 1) {
@@ -513,6 +604,16 @@ int gemm_swiglu_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
                      cudaStream_t st) {
   return gemm_impl(A, lda, B, ldb, C, ldc, M, 2 * d_ff, K, nullptr, nullptr, 0, a_rows_alloc, force_bn, force_splits,
                    1, workspace, ws_bytes, st);
+}
+
+int gemm_qkv_rope_bf16(const bf16* A, int lda, const bf16* W, int ldb, const bf16* bias, bf16* qkv, int M, int K,
+                       int n_heads, int n_kv, const int* tok_pos, const int* tok_slot, const float* rope,
+                       bf16* k_cache, bf16* v_cache, int page_size, int a_rows_alloc, int force_bn,
+                       int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st) {
+  const int N = (n_heads + 2 * n_kv) * 128;
+  QkvRopeArgs qa{tok_pos, tok_slot, rope, k_cache, v_cache, n_heads, n_kv, page_size};
+  return gemm_impl(A, lda, W, ldb, qkv, N, M, N, K, bias, nullptr, 0, a_rows_alloc, force_bn, force_splits, 0,
+                   workspace, ws_bytes, st, &qa);
 }
 
 size_t gemm_workspace_bytes(int M, int N, int K) {

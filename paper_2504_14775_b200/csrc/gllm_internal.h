@@ -25,6 +25,12 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, 
 int gemm_swiglu_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int d_ff, int K,
                      int a_rows_alloc, int force_bn, int force_splits, void* workspace, size_t ws_bytes,
                      cudaStream_t st);
+// qkv = A W^T (+bias) with RoPE on q/k and the k/v heads scattered to the paged cache, fused in
+// the GEMM epilogue (q heads land in qkv rows; k/v columns of qkv are left unwritten)
+int gemm_qkv_rope_bf16(const bf16* A, int lda, const bf16* W, int ldb, const bf16* bias, bf16* qkv, int M, int K,
+                       int n_heads, int n_kv, const int* tok_pos, const int* tok_slot, const float* rope,
+                       bf16* k_cache, bf16* v_cache, int page_size, int a_rows_alloc, int force_bn,
+                       int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int M, int N, int K);
 // bf16 [rows, cols] (leading dim ld) as a TMA map with 64-col x box_rows boxes, 128B swizzle (cached)
 int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);

@@ -3,7 +3,7 @@
 // gllm_stage_forward runs one micro-batch through this stage's layers with
 // one host call (no per-kernel Python round trips): metadata apply + device
 // slot mapping, embedding (first stage), then per layer
-//   RMSNorm -> QKV GEMM(+bias) -> RoPE + paged KV write -> mixed paged attention
+//   RMSNorm -> QKV GEMM(+bias, RoPE + paged KV write fused in its epilogue) -> mixed paged attention
 //   -> O GEMM(+residual) -> RMSNorm -> gate-up GEMM with fused SiLU*mul -> down GEMM(+residual)
 // and on the last stage final RMSNorm of the emitting rows -> LM head GEMM -> argmax.
 // This is the real work behind the reference's `stage_time()` stand-in
@@ -245,17 +245,14 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
     if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
                         [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.attn_norm, w.h, T, D, d.rms_eps, st); })))
       return rc;
-    if ((rc = prof_call(P_GEMM_QKV, 2.0 * Td * Qd * Dd, gemm_bytes(Td, Qd, Dd, false, L.b_qkv != nullptr), st, [&] {
-           return gemm_bf16(w.h, D, (const bf16*)L.w_qkv, D, w.qkv, qkv_w, T, qkv_w, D, (const bf16*)L.b_qkv, nullptr,
-                            0, maxT, 0, 0, w.gemm, w.gemm_bytes, st);
+    // QKV GEMM (+bias) with RoPE and the paged K/V write fused into its epilogue
+    if ((rc = prof_call(P_GEMM_QKV, 2.0 * Td * Qd * Dd,
+                        gemm_bytes(Td, Qd, Dd, false, L.b_qkv != nullptr) + Td * 2.0 * KV * HDIM * 2.0, st, [&] {
+           return gemm_qkv_rope_bf16(w.h, D, (const bf16*)L.w_qkv, D, (const bf16*)L.b_qkv, w.qkv, T, D, H, KV,
+                                     w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, maxT, 0, 0, w.gemm,
+                                     w.gemm_bytes, st);
          })))
       return rc;
-    GLLM_CHECK(w.qkv, (size_t)T * qkv_w, "gemm_qkv", l);
-    if ((rc = prof_call(P_ROPE_KV, 0, Td * (Qd + Od) * 2.0 + Td * 2.0 * KV * HDIM * 2.0, st, [&] {
-           return rope_kv_write(w.qkv, T, H, KV, HDIM, w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, st);
-         })))
-      return rc;
-    GLLM_CHECK(w.qkv, (size_t)T * qkv_w, "rope_kv_write", l);
     if ((rc = prof_call(P_ATTN, att_flops, att_bytes, st, [&] {
            return attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, B.n_prefill_work, S.block_table,
                                   d.max_pages_per_row, d.num_pages, kc, vc, H, KV, HDIM, d.page_size, w.attn, st);
@@ -349,6 +346,15 @@ int gllm_gemm_swiglu_bf16(const void* A, int lda, const void* B_interleaved, int
                           gllm_stream_t stream) {
   return gemm_swiglu_bf16((const bf16*)A, lda, (const bf16*)B_interleaved, ldb, (bf16*)act, ldc, M, d_ff, K, M,
                           force_bn, force_splits, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_gemm_qkv_rope_bf16(const void* A, int lda, const void* W, int ldb, const void* bias, void* qkv, int M, int K,
+                            int n_heads, int n_kv_heads, const int32_t* tok_pos, const int32_t* tok_slot,
+                            const float* rope, void* k_cache, void* v_cache, int page_size, int force_bn,
+                            int force_splits, void* workspace, size_t workspace_bytes, gllm_stream_t stream) {
+  return gemm_qkv_rope_bf16((const bf16*)A, lda, (const bf16*)W, ldb, (const bf16*)bias, (bf16*)qkv, M, K, n_heads,
+                            n_kv_heads, tok_pos, tok_slot, rope, (bf16*)k_cache, (bf16*)v_cache, page_size, M,
+                            force_bn, force_splits, workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,

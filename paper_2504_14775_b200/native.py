@@ -19,7 +19,8 @@ SEQ_FIELDS = 5
 # Every symbol include/gllm.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "gllm_version", "gllm_last_error", "gllm_attention_q_tile", "gllm_stage_workspace_bytes",
-    "gllm_stage_forward", "gllm_commit_tokens", "gllm_gemm_bf16", "gllm_gemm_swiglu_bf16", "gllm_rmsnorm", "gllm_silu_mul",
+    "gllm_stage_forward", "gllm_commit_tokens", "gllm_gemm_bf16", "gllm_gemm_swiglu_bf16", "gllm_gemm_qkv_rope_bf16",
+    "gllm_rmsnorm", "gllm_silu_mul",
     "gllm_prepare_batch", "gllm_embed", "gllm_rope_kv_write", "gllm_attn_mixed_paged", "gllm_argmax",
     "gllm_launch_count", "gllm_profile_begin", "gllm_profile_end",
 )
@@ -78,6 +79,7 @@ def load() -> C.CDLL:
         "gllm_commit_tokens": (i, [C.POINTER(Stage), C.POINTER(Batch), vp, vp]),
         "gllm_gemm_bf16": (i, [vp, i, vp, i, vp, i, i, i, i, vp, vp, i, i, i, vp, sz, vp]),
         "gllm_gemm_swiglu_bf16": (i, [vp, i, vp, i, vp, i, i, i, i, i, i, vp, sz, vp]),
+        "gllm_gemm_qkv_rope_bf16": (i, [vp, i, vp, i, vp, vp, i, i, i, i, vp, vp, vp, vp, vp, i, i, i, vp, sz, vp]),
         "gllm_rmsnorm": (i, [vp, i, vp, vp, vp, i, i, f, vp]),
         "gllm_silu_mul": (i, [vp, i, vp, i, vp]),
         "gllm_prepare_batch": (i, [C.POINTER(Stage), C.POINTER(Batch), vp, vp, vp, vp, vp]),

@@ -74,6 +74,43 @@ def test_gemm_swiglu_fused(lib, M, d_ff, K):
         assert _rel(act, ref) < 1e-2, (bn, splits, _rel(act, ref))
 
 
+@pytest.mark.parametrize("M,name,splits", [(5, "llama3-8b", 0), (300, "llama3-8b", 0), (2009, "llama3-8b", 1),
+                                           (77, "qwen2.5-14b", 1), (64, "qwen2.5-14b", 0), (130, "tiny", 1)])
+def test_gemm_qkv_rope_fused_matches_unfused(lib, M, name, splits):
+    """Fused QKV+RoPE+KV-write epilogue is bit-identical to GEMM(+bias) -> rope_kv_write."""
+    from paper_2504_14775_b200.modelspec import MODELS, rope_table
+    spec = MODELS[name]
+    H, KV, d, ps = spec.n_heads, spec.n_kv_heads, spec.d_model, 16
+    Q = spec.qkv_width
+    g = torch.Generator(device="cuda").manual_seed(M)
+    A = torch.randn(M, d, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(Q, d, device="cuda", generator=g) * 0.03).bfloat16()
+    bias = torch.randn(Q, device="cuda", generator=g).bfloat16() if spec.qkv_bias else None
+    rope = torch.from_numpy(rope_table(spec, 4096)).cuda()
+    pos = torch.randint(0, 4000, (M,), dtype=torch.int32, device="cuda")
+    slot = torch.randperm(512 * ps, device="cuda")[:M].to(torch.int32)
+    ws = torch.empty(160 << 20, dtype=torch.uint8, device="cuda")
+    st = lib.stream_handle()
+    # unfused reference path
+    ref = torch.empty(M, Q, device="cuda").bfloat16()
+    lib.call("gllm_gemm_bf16", A.data_ptr(), d, W.data_ptr(), d, ref.data_ptr(), Q, M, Q, d,
+             None if bias is None else bias.data_ptr(), None, 0, 0, 0, ws.data_ptr(), ws.numel(), st)
+    kr = torch.zeros(512, KV, ps, 128, device="cuda").bfloat16()
+    vr = torch.zeros_like(kr)
+    lib.call("gllm_rope_kv_write", ref.data_ptr(), M, H, KV, 128, pos.data_ptr(), slot.data_ptr(), rope.data_ptr(),
+             kr.data_ptr(), vr.data_ptr(), ps, st)
+    # fused
+    out = torch.zeros(M, Q, device="cuda").bfloat16()
+    kf = torch.zeros_like(kr)
+    vf = torch.zeros_like(kr)
+    lib.call("gllm_gemm_qkv_rope_bf16", A.data_ptr(), d, W.data_ptr(), d, None if bias is None else bias.data_ptr(),
+             out.data_ptr(), M, d, H, KV, pos.data_ptr(), slot.data_ptr(), rope.data_ptr(), kf.data_ptr(), vf.data_ptr(),
+             ps, 0, splits, ws.data_ptr(), ws.numel(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, : H * 128], ref[:, : H * 128])
+    assert torch.equal(kf, kr) and torch.equal(vf, vr)
+
+
 def test_rmsnorm_and_silu(lib):
     x = torch.randn(37, 4096, device="cuda").bfloat16()
     w = (torch.rand(4096, device="cuda") + 0.5).bfloat16()
