@@ -14,7 +14,8 @@ Reported (one JSON line on rank 0):
   value       output tokens / sum of device time of the K micro-batches
               (CUDA events on the launch stream; metadata already in HBM)
   e2e         same tokens / wall time of the K steps through the public API
-              (host scheduling + pinned H2D metadata + forward + D2H tokens)
+              (host scheduling + pinned H2D metadata + forward + D2H tokens); the
+              serving loop plans batch i+1 while batch i runs (lookahead, serving.py)
   roofline    dominant kernel class from a profiled pass (native CUDA-event profiler)
   cpu_baseline the oracle CPU port (oracle/cpu_path.py) on this host
 With N>1 under torchrun the stages are split across ranks (PP=N, pipeline.py).
@@ -50,6 +51,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--cpu-sample-layers", type=int, default=2)
+    p.add_argument("--no-lookahead", action="store_true", help="wait for each commit before planning the next batch")
     return p.parse_args()
 
 
@@ -171,7 +173,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     init_s = time.time() - t_init
     eng = ServingEngine(reqs, scheduler=args.scheduler, pipeline=PipelineConfig(depth=1),
-                        kv_config=KvConfig(num_pages, page_size), throttle=ThrottleConfig(), executor=ex)
+                        kv_config=KvConfig(num_pages, page_size), throttle=ThrottleConfig(), executor=ex,
+                        lookahead=not args.no_lookahead)
 
     state = {"phase": "warm", "timed_start": None, "timed": [], "commits": 0, "stop": False,
              "warm_iters": 0, "launch0": 0}
@@ -188,9 +191,11 @@ def run_ours(args):
         if st["phase"] == "warmup":
             st["count"] += 1
             if st["count"] >= W:
-                # timed region starts here: nothing in flight (depth 1), device idle after commit
+                # timed region starts here: drain the device (with lookahead one batch is already
+                # queued; its commit is skipped below so only batches launched after t0 count)
                 torch.cuda.synchronize()
                 st["phase"] = "timed"
+                st["skip"] = 0 if args.no_lookahead else 1
                 st["timed_start"] = time.perf_counter()
                 st["t_engine"] = t
                 st["launch0"] = native.launch_count()
@@ -198,6 +203,9 @@ def run_ours(args):
                 clocks.start()
             return
         if st["phase"] == "timed":
+            if st["skip"]:
+                st["skip"] -= 1
+                return
             st["timed"].append((seq, t, n_out))
             if len(st["timed"]) >= K:
                 torch.cuda.synchronize()

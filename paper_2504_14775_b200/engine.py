@@ -327,11 +327,15 @@ class EngineCore:
         _remove_key(self._ready, r.key)
         insort(self._waiting, r.key)
 
-    def _commit(self, t: float, batch: _Batch) -> None:
-        """Last-stage commit (`engine.py:334-364`): decodes first, then prefill chunks."""
+    def _commit(self, t: float, batch: _Batch, retire: bool = True) -> None:
+        """Last-stage commit (`engine.py:334-364`): decodes first, then prefill chunks.
+
+        `retire=False` commits the request state only (the asynchronous serving
+        loop retires the device work later and re-stamps the times, see serving.py).
+        """
         plan = batch.plan
         del self.in_flight[batch.seq]
-        if self.executor is not None:
+        if self.executor is not None and retire:
             self.executor.retire(batch.seq)
         self.committed_tokens += plan.total_tokens
         back: list = []

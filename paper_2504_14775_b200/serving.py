@@ -30,7 +30,7 @@ class ServingEngine(EngineCore):
     def __init__(self, requests, scheduler: str = "throttle", pipeline: PipelineConfig | None = None,
                  kv_config: KvConfig | None = None, throttle: ThrottleConfig | None = None,
                  token_budget: int = 2048, executor=None, max_rows: int | None = None,
-                 time_scale: float = 1.0, record_decisions: bool = False):
+                 time_scale: float = 1.0, record_decisions: bool = False, lookahead: bool = False):
         if executor is None:
             raise ValueError("ServingEngine needs a GPU executor")
         super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget, executor, max_rows)
@@ -42,6 +42,8 @@ class ServingEngine(EngineCore):
         self.decisions: list[tuple] | None = [] if record_decisions else None
         self.commit_log: list[tuple[int, float, int]] = []   # (seq, commit wall ms, sampled tokens)
         self.launch_log: list[tuple[int, float]] = []        # (seq, launch wall ms)
+        self._lookahead = lookahead
+        self._pending: list[tuple] = []   # lookahead: (batch, first-token ids, finished ids) awaiting the device
 
     def now_ms(self) -> float:
         return (time.perf_counter() - self._t0) * 1000.0 * self._time_scale
@@ -75,6 +77,8 @@ class ServingEngine(EngineCore):
 
     def run(self, max_commits: int | None = None, on_commit=None) -> RawRunData:
         """Serve until every request finished (or `max_commits` micro-batches committed)."""
+        if self._lookahead:
+            return self._run_lookahead(max_commits, on_commit)
         ex = self.executor
         self._t0 = time.perf_counter()
         ex.mark_epoch()
@@ -97,6 +101,79 @@ class ServingEngine(EngineCore):
                 commits += 1
                 if on_commit is not None:
                     on_commit(seq, t, n_out)
+                if max_commits is not None and commits >= max_commits:
+                    break
+                continue
+            if self._next_arrival < len(self._arrivals):
+                wait = (self._arrivals[self._next_arrival].arrival_ms - t) / 1000.0 / self._time_scale
+                if wait > 0:
+                    time.sleep(min(wait, 0.05))
+                continue
+            stuck = tuple(sorted(rid for rid, r in self._reqs.items() if not r.finished))
+            raise UnschedulableError(f"no forward progress possible; stuck requests: {list(stuck)}", stuck)
+        ex.synchronize()
+        self._busy = ex.stage_busy_intervals()
+        return self.raw_data()
+
+    # -- asynchronous scheduling -------------------------------------------------------
+    #
+    # Scheduling never reads token values (termination is by output count,
+    # `engine.py:343`), and a batch's device work depends on the previous batch only
+    # through device memory written in stream order (sampled ids -> token history, KV
+    # pages). So right after launching batch i the host can apply batch i's commit to
+    # the request state, plan batch i+1 and enqueue it behind i: the GPU never idles on
+    # host planning. Times are stamped when the device actually finishes a batch.
+    # Every plan is still a Token Throttling decision on the state it saw (decision-
+    # replay parity holds); with lookahead off the loop waits for each commit instead.
+
+    def _launch_ahead(self, t: float) -> bool:
+        if len(self._pending) > self._pipeline.depth or not self.executor.stage0_idle():
+            return False
+        snap = self._decision_snapshot() if self.decisions is not None else None
+        plan = self._try_plan()
+        if plan is None:
+            return False
+        batch = self._make_batch(t, plan)
+        if snap is not None:
+            self.decisions.append((batch.seq, snap, list(plan.decode_ids), list(plan.prefill_chunks)))
+        self.executor.launch(batch.meta)
+        self.launch_log.append((batch.seq, t))
+        ids = batch.meta.ids if batch.meta is not None else plan.decode_ids + [r for r, _ in plan.prefill_chunks]
+        reqs = self._reqs
+        no_first = [rid for rid in ids if reqs[rid].first_ms is None]
+        no_finish = [rid for rid in ids if reqs[rid].finish_ms is None]
+        self._commit(t, batch, retire=False)          # state only; provisional times
+        firsts = [rid for rid in no_first if reqs[rid].first_ms is not None]
+        done = [rid for rid in no_finish if reqs[rid].finish_ms is not None]
+        self._pending.append((batch, firsts, done))
+        return True
+
+    def _run_lookahead(self, max_commits, on_commit) -> RawRunData:
+        ex = self.executor
+        self._t0 = time.perf_counter()
+        ex.mark_epoch()
+        commits = 0
+        while self._unfinished > 0 or self._pending:
+            t = self.now_ms()
+            self._release_arrivals(t)
+            if self._unfinished > 0 and self._launch_ahead(t):
+                continue
+            if self._pending:
+                batch, firsts, done = self._pending.pop(0)
+                ex.wait(batch.seq)
+                ex.retire(batch.seq)
+                t = self.now_ms()
+                self.clock = t
+                self.makespan_ms = max(self.makespan_ms, t)
+                for rid in firsts:
+                    self._reqs[rid].first_ms = t
+                for rid in done:
+                    self._reqs[rid].finish_ms = t
+                n_out = batch.meta.n_emit
+                self.commit_log.append((batch.seq, t, n_out))
+                commits += 1
+                if on_commit is not None:
+                    on_commit(batch.seq, t, n_out)
                 if max_commits is not None and commits >= max_commits:
                     break
                 continue

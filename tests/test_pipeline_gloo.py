@@ -163,3 +163,59 @@ def test_pipeline_end_to_end_gloo(world):
                                         (2, 64, 4, 0.05, "combined"), 2048)
         # the engine may drop decodes by preemption after planning; with 64 pages none happen here
         assert dec == want_dec and chunks == want_chunks, seq
+
+
+def test_lookahead_serving_matches_planner_and_completes():
+    """Asynchronous (lookahead) wall-clock loop on a CPU test double: every decision is the
+    oracle planner on its snapshot, every request gets its tokens, times are monotone."""
+    from oracle.sched_ref import plan
+    from paper_2504_14775_b200.pipeline import HostTransport, MetaChannel, PipelineExecutor  # noqa: F401
+    from paper_2504_14775_b200.serving import ServingEngine
+    from paper_2504_14775_b200.stage import default_prompt_source, pack_batch
+
+    reqs = _requests()
+
+    class Exec:
+        def __init__(self):
+            self.src = default_prompt_source({r.id: r for r in reqs}, SPEC.vocab)
+            self.q, self.outputs = {}, {}
+
+        def launch(self, meta):
+            self.q[meta.seq] = pack_batch(meta, 32, self.src)
+
+        def retire(self, seq):
+            pb = self.q.pop(seq)
+            for rid in pb.emit_ids:
+                self.outputs.setdefault(rid, []).append(0)
+
+        def stage0_idle(self):
+            return True
+
+        def wait(self, seq):
+            pass
+
+        def on_finish(self, rid, row):
+            pass
+
+        def mark_epoch(self):
+            pass
+
+        def synchronize(self):
+            pass
+
+        def stage_busy_intervals(self):
+            return [[]]
+
+    ex = Exec()
+    eng = ServingEngine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(64, 4),
+                        throttle=ThrottleConfig(T=2, min_p=4, max_p=64), executor=ex, record_decisions=True,
+                        lookahead=True, time_scale=50.0)
+    raw = eng.run()
+    for r in raw.requests:
+        assert r.completion_ms is not None and r.first_token_ms is not None
+        assert r.arrival_ms <= r.first_token_ms <= r.completion_ms
+        assert len(ex.outputs[r.id]) == r.output_tokens
+    for seq, (wp, rd, free, waiting, ready, pq, dq), dec, chunks in eng.decisions:
+        want = plan("throttle", wp, rd, free, 64, 4, 1, [(rid, pq[rid][0], pq[rid][1]) for rid in waiting],
+                    [(rid, dq[rid]) for rid in ready], (2, 64, 4, 0.05, "combined"), 2048)
+        assert (dec, chunks) == want[:2], seq
