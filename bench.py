@@ -46,12 +46,15 @@ def parse():
     p.add_argument("--n-requests", type=int, default=2000)
     p.add_argument("--rate", type=float, default=2000.0, help="Poisson arrivals per second")
     p.add_argument("--scheduler", default="throttle", choices=["throttle", "sarathi"])
+    p.add_argument("--trace", default="sharegpt", choices=["sharegpt", "azure", "c5"],
+                   help="length distribution: ShareGPT-like (C2-C4), Azure-like, or C5 long prompts (4-8k)")
     p.add_argument("--warm-decodes", type=int, default=1024, help="untimed warm-in until this many decodes run")
     p.add_argument("--warm-max-iters", type=int, default=400)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--cpu-sample-layers", type=int, default=2)
     p.add_argument("--no-lookahead", action="store_true", help="wait for each commit before planning the next batch")
+    p.add_argument("--report-dir", default="", help="write report.json / requests.csv / iterations.csv of the GPU run")
     return p.parse_args()
 
 
@@ -113,9 +116,13 @@ class ClockSampler:
 
 
 def make_trace(args):
-    from paper_2504_14775_b200.workload import ArrivalProcess, builtin_length_table, synthesize_requests
-    return synthesize_requests(ArrivalProcess.poisson(args.rate, 0), builtin_length_table("sharegpt-like"),
-                               args.n_requests)
+    from paper_2504_14775_b200.workload import (ArrivalProcess, LengthDistribution, builtin_length_table,
+                                                synthesize_requests)
+    if args.trace == "c5":   # prompts 4096..8192 step 128, outputs 100..500
+        dist = LengthDistribution.empirical([(p, o) for p in range(4096, 8193, 128) for o in (100, 200, 300, 400, 500)])
+    else:
+        dist = builtin_length_table("azure-like" if args.trace == "azure" else "sharegpt-like")
+    return synthesize_requests(ArrivalProcess.poisson(args.rate, 0), dist, args.n_requests)
 
 
 def roofline(profile: dict, peaks: dict) -> dict:
@@ -187,6 +194,7 @@ def run_ours(args):
             st["warm_iters"] += 1
             if eng._rd >= args.warm_decodes or st["warm_iters"] >= args.warm_max_iters:
                 st["phase"], st["count"] = "warmup", 0
+                clocks.start()   # sampler running before (and throughout) the timed region
             return
         if st["phase"] == "warmup":
             st["count"] += 1
@@ -200,7 +208,6 @@ def run_ours(args):
                 st["t_engine"] = t
                 st["launch0"] = native.launch_count()
                 torch.cuda.nvtx.range_push("bench_timed")   # ncu --nvtx --nvtx-include bench_timed/
-                clocks.start()
             return
         if st["phase"] == "timed":
             if st["skip"]:
@@ -261,14 +268,24 @@ def run_ours(args):
         "h2d_bytes_per_step": ex.h2d_bytes_total_for([s for s, _, _ in timed]) / K,
         "d2h_bytes_per_step": 4.0 * out_tokens / K,
     }
+    # cost-model calibration: fit the reference StageCostModel to measured stages
+    from paper_2504_14775_b200.calibration import fit_stage_cost
+    its = {it.batch_seq: it for it in raw.iterations}
+    seqs = [s for s in dev_ms if s in its and s in eng._ctx_log]
+    if len(seqs) >= 3:
+        model, diag = fit_stage_cost([its[s].total_tokens for s in seqs], [eng._ctx_log[s] for s in seqs],
+                                     [dev_ms[s] for s in seqs])
+        res["calibration"] = {"c0": model.c0, "c_tok": model.c_tok, "c_ctx": model.c_ctx, **diag}
+    if args.report_dir:
+        from paper_2504_14775_b200.metrics import write_report
+        write_report(rep, args.report_dir, extended=True)
     return res, spec
 
 
 def cpu_baseline(args, spec):
     from oracle.cpu_path import run_cpu_path
     from paper_2504_14775_b200.workload import ArrivalProcess, builtin_length_table, synthesize_requests
-    reqs = synthesize_requests(ArrivalProcess.poisson(args.rate, 0), builtin_length_table("sharegpt-like"),
-                               args.n_requests)
+    reqs = make_trace(args)
     return run_cpu_path(spec, reqs, steps=3, warmup=1, sample_layers=args.cpu_sample_layers, time_budget_s=60.0,
                         warm_decodes=args.warm_decodes, warm_max_iters=args.warm_max_iters)
 
@@ -314,7 +331,8 @@ def main():
         "steps": K, "warmup": args.warmup, "ms_per_step": round(res["wall_s"] * 1000 / K, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights, seeded ShareGPT-like trace, PCG64 prompt tokens)",
-        "config": {"workload": f"C2: {args.model} PP=1 on 1xB200, ShareGPT-like, Poisson {args.rate}/s x "
+        "config": {"workload": f"{'C2: ' if args.model == 'llama3-8b' and args.trace == 'sharegpt' else ''}"
+                               f"{args.model} PP=1 on 1xB200, {args.trace} lengths, Poisson {args.rate}/s x "
                                f"{args.n_requests} requests, {args.scheduler} T=8 MaxP=2048 MinP=32 thr=0.05",
                    "model": args.model, "parallelism": "pp1", "page_size": 16, "kv_pages": res["num_pages"],
                    "tokens_per_step": round(res["tokens_per_step"], 1),
@@ -328,8 +346,10 @@ def main():
         "clocks": res["clocks"],
         "serving": {"p50_ttft_ms": rep.ttft_p50_ms, "p50_tpot_ms": rep.tpot_p50_ms,
                     "bubble_frac": res["bubble"], "finished": rep.finished_requests,
+                    "token_stddev_per_iter": rep.token_stddev, "token_mean_per_iter": rep.token_mean,
                     "note": "latency stats over requests finished during the run (overloaded arrival rate)"},
         "profile": {k: {"launches": v["launches"], "ms": round(v["total_ms"], 3)} for k, v in (res["profile"] or {}).items()},
+        "calibration": res.get("calibration"),
     }
     print(json.dumps(line))
     return 0

@@ -274,6 +274,7 @@ class EngineCore:
         self._events: list[dict] | None = None
         self._seq = 0
         self._pending_prompts: list[tuple[int, int]] = []
+        self._ctx_log: dict[int, int] = {}   # seq -> decode context tokens (cost-model calibration)
 
     # -- logging ---------------------------------------------------------------
 
@@ -504,6 +505,7 @@ class EngineCore:
         _remove_prefix_ids(self._waiting, [rid for rid, _ in plan.prefill_chunks], reqs)
         self.in_flight[seq] = batch
         self._iters.append(IterationRecord(seq, t, plan.prefill_tokens, plan.decode_tokens))
+        self._ctx_log[seq] = plan.decode_context_tokens
         return batch
 
     # -- results -------------------------------------------------------------------
