@@ -419,9 +419,17 @@ def bench_pipeline(args) -> int:
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    gloo = dist.new_group(backend="gloo")
+    dev_id = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev_id)
+    # GLLM_PP_TRANSPORT=host: activations staged through host memory over gloo (lets all ranks
+    # share one GPU for testing); default: NCCL send/recv between the ranks' GPUs.
+    host_transport = os.environ.get("GLLM_PP_TRANSPORT", "nccl") == "host"
+    if host_transport:
+        dist.init_process_group("gloo")
+        gloo = dist.group.WORLD
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_id))
+        gloo = dist.new_group(backend="gloo")
     spec = MODELS[args.model]
     reqs = synthesize_requests(ArrivalProcess.poisson(args.rate, 0), builtin_length_table("sharegpt-like"),
                                args.n_requests)
@@ -430,6 +438,7 @@ def bench_pipeline(args) -> int:
     layers = len(stage_layers(spec.n_layers, world, 0))
     need_pages = sum(-(-(r.input_tokens + r.output_tokens) // page_size) for r in reqs)
     free, _ = torch.cuda.mem_get_info()
+    free //= max(1, sum(1 for r in range(world) if r % torch.cuda.device_count() == dev_id))  # shared GPU
     w_bytes = layers * spec.params_per_layer * 2 + 2 * spec.vocab * spec.d_model * 2
     page_bytes = layers * spec.kv_bytes_per_token_layer * page_size
     fit = int((free - w_bytes - max_tokens * (10 * spec.d_model + 6 * spec.d_ff) * 2 * 4 - (10 << 30)) // page_bytes)
@@ -437,18 +446,22 @@ def bench_pipeline(args) -> int:
     dist.all_reduce(num_pages, op=dist.ReduceOp.MIN, group=gloo)   # one shared page table: same pool size
     num_pages = int(num_pages.item())
     meta = MetaChannel(gloo, world)
-    transport = NcclTransport()
+    transport = HostTransport(gloo) if host_transport else NcclTransport()
+    from . import native
+    launches0 = native.launch_count()
     dist.barrier(group=gloo)
     if rank != 0:
-        t0 = time.perf_counter()
         out = worker_loop(spec, reqs, rank=rank, world=world, meta=meta, transport=transport, num_pages=num_pages,
-                          page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests)
-        wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
-        dist.all_reduce(wall, op=dist.ReduceOp.MAX, group=gloo)
+                          page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests,
+                          device=f"cuda:{dev_id}")
+        stats = torch.tensor([0.0, float(native.launch_count() - launches0), float(out["batches"])],
+                             dtype=torch.float64)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=gloo)
         dist.destroy_process_group()
         return 0
     ex = PipelineExecutor(spec, reqs, world=world, meta=meta, transport=transport, num_pages=num_pages,
-                          page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests)
+                          page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests,
+                          device=f"cuda:{dev_id}")
     eng = ServingEngine(reqs, scheduler=args.scheduler, pipeline=PipelineConfig(depth=world),
                         kv_config=KvConfig(num_pages, page_size), throttle=ThrottleConfig(), executor=ex)
     st = {"phase": "warm", "n": 0, "timed": []}
@@ -472,13 +485,21 @@ def bench_pipeline(args) -> int:
                 st["t1"] = time.perf_counter()
                 raise _Stop
 
+    from bench import ClockSampler
+    clocks = ClockSampler(dev_id)
+    clocks.start()
     try:
         eng.run(on_commit=hook)
     except _Stop:
         pass
+    clk = clocks.stop()
     ex.shutdown()
-    wall = torch.tensor([st["t1"] - st["t0"]], dtype=torch.float64)
-    dist.all_reduce(wall, op=dist.ReduceOp.MAX, group=gloo)
+    # rank 0's driver clock spans every stage of every timed batch (a batch commits only after
+    # the last rank's tokens arrive), so it is the max over ranks of the pipeline's time.
+    stats = torch.tensor([st["t1"] - st["t0"], float(native.launch_count() - launches0), float(ex.launches)],
+                         dtype=torch.float64)
+    dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=gloo)
+    wall = stats[0:1]
     out_tok = sum(n for _, _, n in st["timed"])
     raw = eng.raw_data()
     rep = build_report(raw)
@@ -491,7 +512,8 @@ def bench_pipeline(args) -> int:
             "e2e": {"value": round(out_tok / wall.item(), 2), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(ex.h2d_bytes_total_for([s for s, _, _ in st["timed"]]) / max(K, 1)),
                     "d2h_bytes_per_step": int(4 * out_tok / max(K, 1))},
-            "gpu_launches": None,
+            "gpu_launches": int(stats[1].item()), "clocks": clk,
+            "transport": "host-staged gloo (test)" if host_transport else "nccl p2p",
             "serving": {"p50_ttft_ms": rep.ttft_p50_ms, "p50_tpot_ms": rep.tpot_p50_ms,
                         "decodes_per_step": statistics.mean(eng._iters[s].decode_tokens for s, _, _ in st["timed"])}}
     print(json.dumps(line))
