@@ -12,16 +12,20 @@
 //    HMMA tile (mma.sync m16n8k16: this GEMV-shaped work is too small for a
 //    128-row tcgen05 tile), online softmax on lane quads, warps merged through
 //    shared memory. HBM-bound by design.
-//  * prefill role (tensor cores): 128 (token, head) rows of one chunk
-//    (QT = 128/G tokens x the G heads sharing the kv head) against its cached
-//    prefix + its own earlier tokens in 64-key blocks. S = Q.K^T and O += P.V
-//    are tcgen05.mma (M=128) with S and O accumulating in TMEM; each thread
-//    owns one row (TMEM lane), so the causal mask and online softmax are
-//    thread-local. Q/K/V/P are staged in 128B-swizzled smem (K-major for Q, K,
-//    P; MN-major descriptor for V, which stays [key][dim] as the cache holds
-//    it). K blocks are double-buffered with cp.async (prefetched two blocks
-//    ahead), V single-buffered so two CTAs fit per SM; O is rescaled in TMEM only when a row's max grows by >8
-//    (log2 units), the exact "lazy rescale" form of online softmax.
+//  * prefill role (tensor cores, its own launch `attn_prefill_kernel`): a work
+//    item is 2 x 128 (token, head) query rows of one chunk (2 x 128/G tokens x
+//    the G heads sharing the kv head), attended against the cached prefix plus
+//    the chunk's own earlier tokens in 128-key blocks, FlashAttention-style and
+//    warp-specialised: warp 8 streams K/V blocks from the paged cache with 2-D
+//    TMA (one box per page and 64-dim half, 128B-swizzled) into a 4-slot ring;
+//    warp 9 issues every tcgen05.mma (S = Q.K^T with Q, K from smem; O += P.V
+//    with P read straight from TMEM, V as an MN-major smem operand); warps 0-3
+//    and 4-7 run the online softmax of query tile 0 and 1, one thread per TMEM
+//    lane (= query row). The two tiles ping-pong: while one tile's softmax runs
+//    on the CUDA cores the tensor core computes the other tile's P.V and next
+//    S. S/P (aliased, P as packed bf16 over S's first 64 columns) and O take
+//    all 512 TMEM columns; O is rescaled in TMEM only when a row's max grows by
+//    more than 8 (log2 units), the exact "lazy rescale" form of online softmax.
 //
 // Cache layout [page][kv_head][slot][hd] (stage.py); pages resolved through the
 // device block table. Work list: int32 (seq index, q_start) pairs, host-packed.
@@ -37,17 +41,20 @@ constexpr int ATT_THREADS = 128;
 constexpr int NWARP = ATT_THREADS / 32;
 
 // ---------------------------------------------------------------- prefill role
-constexpr int PM = 128;        // query rows per CTA (MMA M)
-constexpr int PBK = 64;        // keys per block (MMA N of S, K of P.V)
-constexpr int TMEM_COLS = 256; // S: cols [0,64), O: cols [128,256)
+constexpr int PM = 128;          // query rows per tile (MMA M = TMEM lanes)
+constexpr int PTILES = 2;        // query tiles per CTA, ping-ponged on the tensor core
+constexpr int PBK = 128;         // keys per block (MMA N of S, MMA K of P.V)
+constexpr int PRING = 4;         // K/V block ring: K_j, V_j, K_j+1, V_j+1
+constexpr int PF_THREADS = 320;  // warps 0-7 softmax (tile = warp / 4), warp 8 TMA, warp 9 MMA
+constexpr int PF_TMEM_COLS = 512;
 constexpr float RESCALE_TH = 8.f;
+constexpr uint32_t PF_BLK_BYTES = PBK * HD * 2;  // one K or V block: two 64-dim SW128 halves
 
 struct PrefillSmem {
-  __align__(1024) uint8_t q[2][PM * 128];        // two 64-dim halves, SW128 K-major
-  __align__(1024) uint8_t k[2][2][PBK * 128];    // [buf][half]
-  __align__(1024) uint8_t v[2][PBK * 128];       // [half] (single buffer: keeps 2 CTAs/SM)
-  __align__(1024) uint8_t p[PM * 128];           // P [128 rows][64 keys] bf16, SW128 K-major
-  uint64_t s_bar, pv_bar;
+  __align__(1024) uint8_t q[PTILES][2][PM * 128];   // [tile][64-dim half], SW128 K-major
+  __align__(1024) uint8_t kv[PRING][2][PBK * 128];  // [slot][64-dim half], key rows
+  uint64_t kv_full[PRING], kv_empty[PRING];
+  uint64_t s_full[PTILES], p_full[PTILES], o_full[PTILES];
   uint32_t tmem_base;
 };
 
@@ -281,201 +288,297 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
 }
 
 
-// One 128-row query tile of a prefill chunk on the tensor cores (see file header).
-template <int G>
-__device__ __forceinline__ void prefill_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok_off, int start,
-                                             int q0, int nq, const int* __restrict__ table,
-                                             const bf16* __restrict__ k_cache, const bf16* __restrict__ v_cache,
-                                             int n_heads, int n_kv, int kvh, int page_size, float scale_log2,
-                                             bf16* __restrict__ out) {
-  PrefillSmem& sm = *reinterpret_cast<PrefillSmem*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int R = nq * G;
-  const int kv_len = start + q0 + nq;
-  const int qkv_w = (n_heads + 2 * n_kv) * HD;
-  const size_t head_stride = (size_t)page_size * HD;
-  const int nb = (kv_len + PBK - 1) / PBK;
+GLLM_DEVICE float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
-  if (tid == 0) {
-    mbar_init(&sm.s_bar, 1);
-    mbar_init(&sm.pv_bar, 1);
+// D[tmem] (+)= A[tmem] * B[smem]: the A operand (P, 128 rows x K bf16, two per 32-bit column)
+// is read from tensor memory.
+GLLM_DEVICE void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// Prefill chunks on the tensor cores (see the file header). Work item = (sequence, q0): query
+// tokens [q0, q0 + 2*QT) of the chunk as two 128-row tiles; grid = (kv head, item).
+template <int G>
+__global__ void __launch_bounds__(PF_THREADS, 1)
+attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
+                    const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
+                    int n_work, const int* __restrict__ block_table, int mpr, int n_heads, int n_kv, int page_size,
+                    float scale_log2, bf16* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t smem_dyn[];
+  PrefillSmem& sm =
+      *reinterpret_cast<PrefillSmem*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  constexpr int QT = PM / G;  // query tokens per tile
+  const int kvh = blockIdx.x;
+  const int item = n_work - 1 - (int)blockIdx.y;  // a chunk's later (longer) tiles start first
+  const int sidx = work[2 * item], q0 = work[2 * item + 1];
+  const int* si = seq_info + 5 * sidx;
+  const int row_id = si[0], start = si[1], n_new = si[2], tok_off = si[3];
+  const int* table = block_table + (size_t)row_id * mpr;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qkv_w = (n_heads + 2 * n_kv) * HD;
+
+  int nq[PTILES], nblk[PTILES];
+#pragma unroll
+  for (int t = 0; t < PTILES; ++t) {
+    nq[t] = max(0, min(QT, n_new - (q0 + t * QT)));
+    nblk[t] = nq[t] > 0 ? (start + q0 + t * QT + nq[t] + PBK - 1) / PBK : 0;
+  }
+  const int kv_len = start + q0 + nq[0] + nq[1];  // keys of the item's last query
+  const int nb = max(nblk[0], nblk[1]);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PRING; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int t = 0; t < PTILES; ++t) {
+      mbar_init(&sm.s_full[t], 1);
+      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.o_full[t], 1);
+    }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc(&sm.tmem_base, TMEM_COLS);
-
-  // Q tile -> swizzled smem (rows >= R zero-filled).
-  for (int i = tid; i < PM * 16; i += ATT_THREADS) {
-    const int r = i >> 4, c16 = i & 15, half = c16 >> 3, c = c16 & 7;
-    uint8_t* dst = sm.q[half] + sw128_off(r, c);
-    if (r < R) {
-      const int qi = r / G, gh = r % G;
-      cp_async16(dst, qkv + (size_t)(tok_off + q0 + qi) * qkv_w + (kvh * G + gh) * HD + half * 64 + c * 8);
-    } else {
-      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+  if (warp == 0) tmem_alloc(&sm.tmem_base, PF_TMEM_COLS);
+  if (warp < 8) {
+    // Q tiles -> swizzled smem; tile row r = (token r / G, head r % G) of this kv head's group
+    for (int i = threadIdx.x; i < PTILES * PM * 16; i += 256) {
+      const int t = i / (PM * 16), r = (i >> 4) % PM, c16 = i & 15, half = c16 >> 3, c = c16 & 7;
+      uint8_t* dst = sm.q[t][half] + sw128_off(r, c);
+      if (r < nq[t] * G) {
+        const int qi = r / G, gh = r % G;
+        cp_async16(dst, qkv + (size_t)(tok_off + q0 + t * QT + qi) * qkv_w + (kvh * G + gh) * HD + half * 64 + c * 8);
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      }
     }
+    cp_async_commit();
+    cp_async_wait<0>();
+    fence_proxy_async();
   }
-  auto load_kv = [&](const bf16* cache, uint8_t (*buf)[PBK * 128], int blk) {
-    // 64 keys x 16 chunks of 16 B; 8 per thread
-#pragma unroll
-    for (int j = 0; j < (PBK * 16) / ATT_THREADS; ++j) {
-      const int i = tid + j * ATT_THREADS;
-      const int kk = i >> 4, c16 = i & 15, half = c16 >> 3, c = c16 & 7;
-      int key = blk * PBK + kk;
-      if (key >= kv_len) key = kv_len - 1;  // clamped duplicate, masked in softmax
-      const int page = table[key / page_size];
-      const bf16* src = cache + ((size_t)page * n_kv + kvh) * head_stride + (size_t)(key % page_size) * HD + half * 64 + c * 8;
-      cp_async16(buf[half] + sw128_off(kk, c), src);
-    }
-  };
-  // prologue groups: [Q, K0], [K1]
-  load_kv(k_cache, sm.k[0], 0);
-  cp_async_commit();
-  if (nb > 1) load_kv(k_cache, sm.k[1], 1);
-  cp_async_commit();
-  cp_async_wait<1>();
-  fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const uint32_t t_s = tmem, t_o = tmem + 128;
-  constexpr uint32_t idesc_s = idesc_bf16_f32(PM, PBK);
-  constexpr uint32_t idesc_o = idesc_bf16_f32(PM, HD, /*b_mn_major=*/true);
 
-  auto issue_s = [&](int blk) {
-    const int b = blk & 1;
-#pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      const int half = kk >> 2;
-      const uint64_t da = smem_desc_sw128(sm.q[half]) + 2 * (kk & 3);
-      const uint64_t db = smem_desc_sw128(sm.k[b][half]) + 2 * (kk & 3);
-      mma_bf16_ss(t_s, da, db, idesc_s, kk > 0 ? 1u : 0u);
-    }
-    mma_commit(&sm.s_bar);
-  };
-  if (tid == 0) issue_s(0);
-
-  // per-row state: this thread owns TMEM lane / query row `tid`
-  const int row = tid;
-  const int qpos = start + q0 + (row < R ? row / G : nq - 1);
-  float m_ref = -FLT_MAX, l_sum = 0.f;
-
-  for (int j = 0; j < nb; ++j) {
-    mbar_wait(&sm.s_bar, j & 1);
-    tc_fence_after();
-    uint32_t s_raw[2][32];
-    tmem_ld_32x32b_x32(t_s + ((uint32_t)(warp * 32) << 16), s_raw[0]);
-    tmem_ld_32x32b_x32(t_s + ((uint32_t)(warp * 32) << 16) + 32, s_raw[1]);
-    tmem_ld_wait();
-    float s[PBK];
-    float mb = -FLT_MAX;
-#pragma unroll
-    for (int c = 0; c < PBK; ++c) {
-      const int kpos = j * PBK + c;
-      float x = __uint_as_float(s_raw[c >> 5][c & 31]) * scale_log2;
-      x = (kpos > qpos || kpos >= kv_len) ? -FLT_MAX : x;
-      s[c] = x;
-      mb = fmaxf(mb, x);
-    }
-    if (j > 0) mbar_wait(&sm.pv_bar, (j - 1) & 1);  // P smem free, O stable, V buffer free
-    tc_fence_after();
-    load_kv(v_cache, sm.v, j);
-    cp_async_commit();
-    // prefetch K for block j+2 into the buffer S_j just finished reading
-    if (j + 2 < nb) load_kv(k_cache, sm.k[j & 1], j + 2);
-    cp_async_commit();
-    // lazy rescale: keep the reference max unless this block exceeds it by > RESCALE_TH.
-    // The decision is per row, but tcgen05.ld/st are warp-collective, so the TMEM
-    // round trip runs for the whole warp whenever any of its rows rescales.
-    const bool grow = mb > m_ref + RESCALE_TH || m_ref == -FLT_MAX;
-    float corr = 1.f;
-    if (grow) {
-      corr = (m_ref == -FLT_MAX) ? 0.f : exp2f(m_ref - mb);
-      l_sum *= corr;
-      m_ref = mb;
-    }
-    if (j > 0 && __any_sync(0xffffffffu, grow && corr != 1.f)) {
-#pragma unroll
-      for (int c = 0; c < HD; c += 32) {
-        uint32_t o[32];
-        const uint32_t ta = t_o + ((uint32_t)(warp * 32) << 16) + c;
-        tmem_ld_32x32b_x32(ta, o);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-        tmem_st_32x32b_x32(ta, o);
+  if (warp == 8) {
+    // ---- TMA producer: fill f = 2j loads K_j, f = 2j+1 loads V_j
+    if (lane == 0) {
+      const int n_pages = (kv_len + page_size - 1) / page_size;
+      const int ppb = PBK / page_size;
+      const uint32_t box_bytes = (uint32_t)page_size * 128;
+      for (int f = 0; f < 2 * nb; ++f) {
+        const int s = f % PRING;
+        if (f >= PRING) mbar_wait(&sm.kv_empty[s], ((f / PRING) + 1) & 1);
+        mbar_arrive_expect_tx(&sm.kv_full[s], PF_BLK_BYTES);
+        const CUtensorMap* m = (f & 1) ? &v_map : &k_map;
+        const int j = f >> 1;
+        for (int pl = 0; pl < ppb; ++pl) {
+          // pages past the item's last key repeat its last page (never an unmapped table entry)
+          const int p = min(j * ppb + pl, n_pages - 1);
+          const int row0 = (table[p] * n_kv + kvh) * page_size;
+          tma_load_2d(m, &sm.kv_full[s], sm.kv[s][0] + pl * box_bytes, 0, row0);
+          tma_load_2d(m, &sm.kv_full[s], sm.kv[s][1] + pl * box_bytes, 64, row0);
+        }
       }
-      tmem_st_wait();
     }
-    // P = exp2(s - m_ref) -> bf16, swizzled K-major row of 64 keys
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      float pv[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float x = s[c * 8 + e];
-        pv[e] = (x == -FLT_MAX) ? 0.f : exp2f(x - m_ref);
-        l_sum += pv[e];
-      }
-      *reinterpret_cast<uint4*>(sm.p + sw128_off(row, c)) =
-          make_uint4(pack_bf16x2(pv[0], pv[1]), pack_bf16x2(pv[2], pv[3]), pack_bf16x2(pv[4], pv[5]),
-                     pack_bf16x2(pv[6], pv[7]));
-    }
-    cp_async_wait<1>();  // V_j and K_{j+1} have landed (this thread's copies); K_{j+2} may fly
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
+  } else if (warp == 9) {
+    // ---- MMA issuer: the warp walks the schedule, lane 0 issues
+    constexpr uint32_t idesc_s = idesc_bf16_f32(PM, PBK);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(PM, HD, /*b_mn_major=*/true);
+    auto wait_full = [&](int f) {
+      mbar_wait(&sm.kv_full[f % PRING], (uint32_t)((f / PRING) & 1));
       tc_fence_after();
+    };
+    auto release = [&](int f) {
+      if (lane == 0) mma_commit(&sm.kv_empty[f % PRING]);
+      __syncwarp();
+    };
+    auto issue_s = [&](int t, int j) {  // S_t = Q_t . K_j^T
+      const int s = (2 * j) % PRING;
+      if (lane == 0) {
 #pragma unroll
-      for (int kk = 0; kk < PBK / 16; ++kk) {
-        const uint64_t da = smem_desc_sw128(sm.p) + 2 * kk;
-        const uint64_t db = smem_desc_sw128_mn(sm.v[0] + kk * 2048, PBK * 128);
-        mma_bf16_ss(t_o, da, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint64_t da = smem_desc_sw128(sm.q[t][kk >> 2]) + 2 * (kk & 3);
+          const uint64_t db = smem_desc_sw128(sm.kv[s][kk >> 2]) + 2 * (kk & 3);
+          mma_bf16_ss(tmem + t * 256, da, db, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm.s_full[t]);
       }
-      mma_commit(&sm.pv_bar);
-      if (j + 1 < nb) issue_s(j + 1);
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t . V_j, P (bf16) in S_t's first 64 columns
+      const int s = (2 * j + 1) % PRING;
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < PBK / 16; ++kk) {
+          const uint64_t db = smem_desc_sw128_mn(sm.kv[s][0] + kk * 2048, PBK * 128);
+          mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+    };
+    wait_full(0);
+    for (int t = 0; t < PTILES; ++t)
+      if (nblk[t] > 0) issue_s(t, 0);
+    release(0);
+    for (int j = 0; j < nb; ++j) {
+      wait_full(2 * j + 1);
+      if (j == nb - 1 && kv_len < nb * PBK) {
+        // keys past the item's last query are never attended, but stale cache slots may hold
+        // NaN/Inf bytes and P = 0 times NaN would poison O: zero those V rows
+        const int s = (2 * j + 1) % PRING;
+        const int k0 = kv_len - j * PBK;
+        for (int i = lane; i < (PBK - k0) * 16; i += 32) {
+          const int r = k0 + (i >> 4), half = (i >> 3) & 1, c = i & 7;
+          *reinterpret_cast<uint4*>(sm.kv[s][half] + sw128_off(r, c)) = make_uint4(0, 0, 0, 0);
+        }
+        fence_proxy_async();
+        __syncwarp();
+      }
+      const bool next = j + 1 < nb;
+      if (next) wait_full(2 * j + 2);
+      for (int t = 0; t < PTILES; ++t) {
+        if (j >= nblk[t]) continue;
+        mbar_wait(&sm.p_full[t], (uint32_t)(j & 1));
+        tc_fence_after();
+        issue_pv(t, j);
+        if (j + 1 < nblk[t]) {
+          issue_s(t, j + 1);
+        } else {
+          if (lane == 0) mma_commit(&sm.o_full[t]);
+          __syncwarp();
+        }
+      }
+      release(2 * j + 1);
+      if (next) release(2 * j + 2);
     }
-  }
-  mbar_wait(&sm.pv_bar, (nb - 1) & 1);
-  tc_fence_after();
-  const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
-  const int qi = row / G, gh = row % G;
-  bf16* o = out + (size_t)(tok_off + q0 + qi) * (n_heads * HD) + (kvh * G + gh) * HD;
+  } else {
+    // ---- softmax + epilogue of tile t: this thread owns TMEM lane / query row `row`
+    const int t = warp >> 2;
+    const int tnq = t ? nq[1] : nq[0], tnb = t ? nblk[1] : nblk[0];
+    if (tnq > 0) {
+      const int row = (warp & 3) * 32 + lane;
+      const uint32_t t_s = tmem + t * 256 + ((uint32_t)((warp & 3) * 32) << 16);
+      const uint32_t t_o = t_s + 128;
+      const int R = tnq * G;
+      const int qfirst = start + q0 + t * QT;
+      const int qpos = qfirst + (row < R ? row / G : tnq - 1);
+      float m_ref = -FLT_MAX, l_sum = 0.f;
+      for (int j = 0; j < tnb; ++j) {
+        mbar_wait(&sm.s_full[t], (uint32_t)(j & 1));
+        tc_fence_after();
+        // pass 1: row max over the block (diagonal blocks mask keys after this row's token by
+        // position, so stale bytes in unattended slots never reach the max)
+        const bool diag = (j + 1) * PBK - 1 > qfirst;
+        const int kmax = qpos - j * PBK;  // keys c <= kmax are attended
+        float mb = -FLT_MAX;
+#pragma unroll 1
+        for (int c0 = 0; c0 < PBK; c0 += 32) {
+          uint32_t s[32];
+          tmem_ld_32x32b_x32(t_s + c0, s);
+          tmem_ld_wait();
+          if (diag) {
 #pragma unroll
-  for (int c = 0; c < HD; c += 32) {
-    uint32_t r32[32];
-    tmem_ld_32x32b_x32(t_o + ((uint32_t)(warp * 32) << 16) + c, r32);  // warp-collective: all lanes
-    tmem_ld_wait();
-    if (row < R) {
+            for (int c = 0; c < 32; ++c) mb = fmaxf(mb, c0 + c <= kmax ? __uint_as_float(s[c]) : -FLT_MAX);
+          } else {
 #pragma unroll
-      for (int e = 0; e < 32; e += 8)
-        *reinterpret_cast<uint4*>(o + c + e) = make_uint4(
-            pack_bf16x2(__uint_as_float(r32[e]) * inv, __uint_as_float(r32[e + 1]) * inv),
-            pack_bf16x2(__uint_as_float(r32[e + 2]) * inv, __uint_as_float(r32[e + 3]) * inv),
-            pack_bf16x2(__uint_as_float(r32[e + 4]) * inv, __uint_as_float(r32[e + 5]) * inv),
-            pack_bf16x2(__uint_as_float(r32[e + 6]) * inv, __uint_as_float(r32[e + 7]) * inv));
+            for (int c = 0; c < 32; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
+          }
+        }
+        mb *= scale_log2;
+        const bool grow = mb > m_ref + RESCALE_TH || m_ref == -FLT_MAX;
+        float corr = 1.f;
+        if (grow) {
+          corr = (m_ref == -FLT_MAX) ? 0.f : ex2_approx(m_ref - mb);
+          l_sum *= corr;
+          m_ref = mb;
+        }
+        // O (complete through block j-1: S_t(j) was issued after P.V_t(j-1)) rescaled in TMEM;
+        // tcgen05.ld/st are warp-collective, so the whole warp joins when any row grows
+        if (j > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(t_o + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st_32x32b_x32(t_o + c, o);
+          }
+        }
+        // pass 2: P = exp2(s * scale - m) as packed bf16 over S's first 64 columns (the 64
+        // columns of keys [64h, 64h + 64) are read before P's columns [32h, 32h + 32) are written)
+        const float neg = -m_ref;
+#pragma unroll 1
+        for (int h = 0; h < PBK / 64; ++h) {
+          uint32_t s0[32], s1[32], pk[32];
+          tmem_ld_32x32b_x32(t_s + h * 64, s0);
+          tmem_ld_32x32b_x32(t_s + h * 64 + 32, s1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t* src2 = e < 16 ? s0 : s1;
+            const int c = h * 64 + 2 * e;
+            float a = ex2_approx(fmaf(__uint_as_float(src2[(2 * e) & 31]), scale_log2, neg));
+            float b = ex2_approx(fmaf(__uint_as_float(src2[(2 * e + 1) & 31]), scale_log2, neg));
+            if (diag) {
+              a = c <= kmax ? a : 0.f;
+              b = c + 1 <= kmax ? b : 0.f;
+            }
+            l_sum += a + b;
+            pk[e] = pack_bf16x2(a, b);
+          }
+          tmem_st_32x32b_x32(t_s + h * 32, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[t]);
+      }
+      mbar_wait(&sm.o_full[t], 0);
+      tc_fence_after();
+      const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
+      const int qi = row / G, gh = row % G;
+      bf16* o = out + (size_t)(tok_off + q0 + t * QT + qi) * (n_heads * HD) + (kvh * G + gh) * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t r32[32];
+        tmem_ld_32x32b_x32(t_o + c, r32);
+        tmem_ld_wait();
+        if (row < R) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 8)
+            *reinterpret_cast<uint4*>(o + c + e) = make_uint4(
+                pack_bf16x2(__uint_as_float(r32[e]) * inv, __uint_as_float(r32[e + 1]) * inv),
+                pack_bf16x2(__uint_as_float(r32[e + 2]) * inv, __uint_as_float(r32[e + 3]) * inv),
+                pack_bf16x2(__uint_as_float(r32[e + 4]) * inv, __uint_as_float(r32[e + 5]) * inv),
+                pack_bf16x2(__uint_as_float(r32[e + 6]) * inv, __uint_as_float(r32[e + 7]) * inv));
+        }
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 0) tmem_dealloc(tmem, PF_TMEM_COLS);
 }
 
 
-// A mixed micro-batch is issued as two concurrent launches (prefill tiles on a forked side
-// stream, decodes on the caller's stream, joined by an event): a single fused launch measured
-// 3.96 resident warps/SM instead of 8 (ncu), because the TMEM-allocating prefill role caps the
-// kernel at one resident CTA per SM, which halves the decode stream's bytes in flight.
-enum AttnRoles { ROLES_PREFILL_ONLY = 0, ROLES_DECODE_ONLY = 1 };
-
-template <int G, int ROLES>
+// A mixed micro-batch is issued as two concurrent launches (prefill items on a forked side
+// stream, decodes on the caller's stream, joined by an event): the prefill kernel takes all of
+// an SM's TMEM and most of its smem, while decode CTAs want two per SM for bytes in flight.
+template <int G>
 __global__ void __launch_bounds__(ATT_THREADS, 2)
-attn_mixed_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
-                  const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
-                  const int* __restrict__ block_table, int mpr, const bf16* __restrict__ k_cache,
-                  const bf16* __restrict__ v_cache, int n_heads, int n_kv, int page_size, float scale_log2,
-                  bf16* __restrict__ out) {
+attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
+                   const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
+                   const int* __restrict__ block_table, int mpr, int n_heads, int n_kv, int page_size,
+                   float scale_log2, bf16* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   const int kvh = blockIdx.x;   // kv heads fastest: a work item's CTAs launch together
@@ -483,44 +586,45 @@ attn_mixed_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_consta
   const int sidx = work[2 * item];
   const int q0 = work[2 * item + 1];
   const int* si = seq_info + 5 * sidx;
-  const int row_id = si[0], start = si[1], n_new = si[2], tok_off = si[3];
+  const int row_id = si[0], start = si[1], tok_off = si[3];
   const int* table = block_table + (size_t)row_id * mpr;
-  if constexpr (ROLES == ROLES_DECODE_ONLY) {
-    decode_role<G>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh,
-                   page_size, scale_log2, out);
-  } else {
-    const int nq = min(PM / G, n_new - q0);
-    prefill_role<G>(smem_raw, qkv, tok_off, start, q0, nq, table, k_cache, v_cache, n_heads, n_kv, kvh, page_size,
-                    scale_log2, out);
-  }
+  decode_role<G>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh, page_size,
+                 scale_log2, out);
 }
 
 // Query tokens per prefill work item (a decode, n_new == 1, is always one item).
-int attention_q_tile(int n_heads, int n_kv) { return PM / (n_heads / n_kv); }
+int attention_q_tile(int n_heads, int n_kv) { return PTILES * (PM / (n_heads / n_kv)); }
 
-template <int G, int ROLES>
+template <bool PREFILL, int G>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
                        int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
                        float scale_log2, bf16* out, cudaStream_t st) {
-  constexpr size_t smem = (ROLES == ROLES_DECODE_ONLY ? sizeof(DecodeSmem) : sizeof(PrefillSmem)) + 1024;
+  constexpr size_t smem = (PREFILL ? sizeof(PrefillSmem) : sizeof(DecodeSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_mixed_kernel<G, ROLES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    const void* fn = PREFILL ? (const void*)attn_prefill_kernel<G> : (const void*)attn_decode_kernel<G>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_cuda_error(e, "attention smem attribute");
-    // all of the unified L1/smem as shared memory: two CTAs (8 streaming warps) per SM
-    e = cudaFuncSetAttribute(attn_mixed_kernel<G, ROLES>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    // all of the unified L1/smem as shared memory (decode: two CTAs, 8 streaming warps per SM)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return set_cuda_error(e, "attention carveout attribute");
     attr = true;
   }
-  // the paged cache viewed as a 2-D [pages*kv_heads*page_size, 128] bf16 tensor for the decode TMA boxes
+  // the paged cache viewed as a 2-D [pages*kv_heads*page_size, 128] bf16 tensor: one TMA box per
+  // (page, kv head, 64-dim half)
   CUtensorMap km, vm;
   if (int rc = make_tma_map_2d(&km, k_cache, (int64_t)kv_pages * n_kv * page_size, HD, HD, page_size)) return rc;
   if (int rc = make_tma_map_2d(&vm, v_cache, (int64_t)kv_pages * n_kv * page_size, HD, HD, page_size)) return rc;
   dim3 grid(n_kv, n_work);
-  attn_mixed_kernel<G, ROLES><<<grid, ATT_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, block_table, mpr, k_cache,
-                                                              v_cache, n_heads, n_kv, page_size, scale_log2, out);
-  return check_launch("attention_mixed");
+  if constexpr (PREFILL) {
+    attn_prefill_kernel<G><<<grid, PF_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, n_work, block_table, mpr,
+                                                            n_heads, n_kv, page_size, scale_log2, out);
+    return check_launch("attention_prefill");
+  } else {
+    attn_decode_kernel<G><<<grid, ATT_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, block_table, mpr, n_heads,
+                                                           n_kv, page_size, scale_log2, out);
+    return check_launch("attention_decode");
+  }
 }
 
 struct AttnStreams {
@@ -543,27 +647,27 @@ static int attn_streams(AttnStreams** out) {
   return 0;
 }
 
-// work[0, n_prefill_work) are prefill tiles, the rest decodes (host packer order).
+// work[0, n_prefill_work) are prefill items, the rest decodes (host packer order).
 template <int G>
 static int launch_attn_g(int n_prefill_work, const bf16* qkv, const int* seq_info, const int* work, int n_work,
                          const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache,
                          int n_heads, int n_kv, int page_size, float scale_log2, bf16* out, cudaStream_t st) {
   const int n_dec = n_work - n_prefill_work;
   if (n_prefill_work == 0)
-    return launch_attn<G, ROLES_DECODE_ONLY>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache,
-                                             n_heads, n_kv, page_size, scale_log2, out, st);
+    return launch_attn<false, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
+                                 n_kv, page_size, scale_log2, out, st);
   if (n_dec == 0)
-    return launch_attn<G, ROLES_PREFILL_ONLY>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache,
-                                              v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    return launch_attn<true, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
+                                n_kv, page_size, scale_log2, out, st);
   AttnStreams* ss = nullptr;
   if (int rc = attn_streams(&ss)) return rc;
   cudaEventRecord(ss->fork, st);
   cudaStreamWaitEvent(ss->side, ss->fork, 0);
-  int rc = launch_attn<G, ROLES_PREFILL_ONLY>(qkv, seq_info, work, n_prefill_work, block_table, mpr, kv_pages, k_cache,
-                                              v_cache, n_heads, n_kv, page_size, scale_log2, out, ss->side);
+  int rc = launch_attn<true, G>(qkv, seq_info, work, n_prefill_work, block_table, mpr, kv_pages, k_cache, v_cache,
+                                n_heads, n_kv, page_size, scale_log2, out, ss->side);
   if (rc == 0)
-    rc = launch_attn<G, ROLES_DECODE_ONLY>(qkv, seq_info, work + 2 * n_prefill_work, n_dec, block_table, mpr,
-                                           kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    rc = launch_attn<false, G>(qkv, seq_info, work + 2 * n_prefill_work, n_dec, block_table, mpr, kv_pages, k_cache,
+                               v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
   cudaEventRecord(ss->join, ss->side);
   cudaStreamWaitEvent(st, ss->join, 0);
   return rc;

@@ -12,7 +12,8 @@ import os
 
 from .errors import NativeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgllm.so")
+# GLLM_LIB: A/B comparisons against another build (tools only); the default is the in-tree library
+LIB_PATH = os.environ.get("GLLM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgllm.so")
 
 SEQ_FIELDS = 5
 

@@ -171,13 +171,18 @@ def _paged_setup(n_kv, hd, ps, ctx_lens, num_pages, seed=0):
     return kc.cuda(), vc.cuda(), table.cuda(), mpr, dense
 
 
-@pytest.mark.parametrize("n_heads,n_kv", [(32, 8), (40, 8), (64, 8), (2, 1)])
-def test_attention_mixed(lib, n_heads, n_kv):
-    hd, ps = 128, 16
+LONG_SEQS = [(37, 1), (1500, 517), (0, 300), (2000, 129), (4, 1), (900, 2)]
+
+
+@pytest.mark.parametrize("n_heads,n_kv,ps,seqs", [(32, 8, 16, None), (40, 8, 16, None), (64, 8, 16, None),
+                                                  (2, 1, 16, None), (32, 8, 16, LONG_SEQS), (40, 8, 8, LONG_SEQS),
+                                                  (64, 8, 16, LONG_SEQS)])
+def test_attention_mixed(lib, n_heads, n_kv, ps, seqs):
+    hd = 128
     # (start, n_new): decodes, a first chunk, a later chunk, a long decode
-    seqs = [(37, 1), (0, 45), (100, 70), (511, 1), (15, 1), (3, 200)]
+    seqs = seqs or [(37, 1), (0, 45), (100, 70), (511, 1), (15, 1), (3, 200)]
     ctx = [s + n for s, n in seqs]
-    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, ctx, num_pages=512)
+    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, ctx, num_pages=sum(-(-c // ps) for c in ctx) + 64)
     T = sum(n for _, n in seqs)
     qkv = torch.randn(T, (n_heads + 2 * n_kv) * hd, device="cuda").bfloat16()
     q_tile = lib.load().gllm_attention_q_tile(n_heads, n_kv)

@@ -32,9 +32,9 @@ def test_exports_match_header(lib):
 
 def test_host_only_entry_points(lib):
     assert lib.gllm_version() >= 1
-    assert lib.gllm_attention_q_tile(32, 8) == 32     # 128 rows / G=4
-    assert lib.gllm_attention_q_tile(40, 8) == 25
-    assert lib.gllm_attention_q_tile(64, 8) == 16
+    assert lib.gllm_attention_q_tile(32, 8) == 64     # 2 tiles x 128 rows / G=4
+    assert lib.gllm_attention_q_tile(40, 8) == 50
+    assert lib.gllm_attention_q_tile(64, 8) == 32
     assert lib.gllm_attention_q_tile(3, 2) == -1
     d = native.Dims(32, 4096, 32, 8, 128, 14336, 128256, 0, 1e-5, 16, 1000, 64, 64, 1024, 3072, 1024)
     assert lib.gllm_stage_workspace_bytes(C.byref(d)) > 3072 * 4096 * 2

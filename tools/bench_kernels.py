@@ -116,6 +116,10 @@ if __name__ == "__main__":
         attn_case("prefill_4x300_from0", [(0, 300)] * 4)
         attn_case("prefill_chunk512_after1500", [(1500, 512)])
         attn_case("mixed_bench", [(500, 1)] * 800 + [(0, 300)] * 3 + [(200, 300)] * 1)
+        attn_case("prefill_2048_from0_8b", [(0, 2048)])
+        attn_case("prefill_2048_after4096_70b", [(4096, 2048)], n_heads=64)
+        attn_case("prefill_640_after6000_70b", [(6000, 640)], n_heads=64)
+        attn_case("prefill_4x512_after2000_qwen", [(2000, 512)] * 4, n_heads=40)
         attn_case("decode256_qwen", [(600, 1)] * 256, n_heads=40)
         attn_case("decode128_70b", [(4000, 1)] * 128, n_heads=64)
     if a.only in ("", "gemm"):
