@@ -294,6 +294,72 @@ GLLM_DEVICE float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (offloads the MUFU unit, which the softmax otherwise saturates):
+// n = rint(x) by the 1.5*2^23 trick, 2^(x-n) with x-n in [-0.5, 0.5] by a degree-3 polynomial
+// (max relative error 1.0e-4, well under bf16's 2^-9 rounding of P), 2^n added to the exponent.
+GLLM_DEVICE float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05500871f, f, 0.24221069f), f, 0.6932829f), f, 1.f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+#ifndef GLLM_EXP2_EMU
+#define GLLM_EXP2_EMU 0   // of every 4 P pairs, this many are exponentiated on the FMA pipe
+#endif
+
+// Packed fp32 pairs (FFMA2 / FADD2 on sm_100): half the issue slots of scalar FFMA / FADD.
+GLLM_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+GLLM_DEVICE float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// P for keys [64h, 64h + 64) of this thread's row: exp2(s * scale - m) packed to bf16 pairs into
+// TMEM columns [32h, 32h + 32) (the S columns of those keys are read before any is overwritten).
+// DIAG: keys c > kmax (after this row's token) are zeroed by position.
+template <bool DIAG>
+GLLM_DEVICE void softmax_p_half(uint32_t t_s, int h, float2 sc2, float2 ng2, int kmax, float2 (&acc)[2]) {
+  uint32_t s0[32], s1[32], pk[32];
+  tmem_ld_32x32b_x32(t_s + h * 64, s0);
+  tmem_ld_32x32b_x32(t_s + h * 64 + 32, s1);
+  tmem_ld_wait();
+#pragma unroll
+  for (int e = 0; e < 32; ++e) {
+    const uint32_t* sv = e < 16 ? s0 : s1;
+    const float2 x = ffma2(make_float2(__uint_as_float(sv[(2 * e) & 31]), __uint_as_float(sv[(2 * e + 1) & 31])), sc2, ng2);
+    float a, b;
+    if ((e & 3) < GLLM_EXP2_EMU) {
+      a = ex2_poly(x.x);
+      b = ex2_poly(x.y);
+    } else {
+      a = ex2_approx(x.x);
+      b = ex2_approx(x.y);
+    }
+    if constexpr (DIAG) {
+      const int c = h * 64 + 2 * e;
+      a = c <= kmax ? a : 0.f;
+      b = c + 1 <= kmax ? b : 0.f;
+    }
+    acc[e & 1] = fadd2(acc[e & 1], make_float2(a, b));
+    pk[e] = pack_bf16x2(a, b);
+  }
+  tmem_st_32x32b_x32(t_s + h * 32, pk);
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]: the A operand (P, 128 rows x K bf16, two per 32-bit column)
 // is read from tensor memory.
 GLLM_DEVICE void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
@@ -479,20 +545,29 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
         // position, so stale bytes in unattended slots never reach the max)
         const bool diag = (j + 1) * PBK - 1 > qfirst;
         const int kmax = qpos - j * PBK;  // keys c <= kmax are attended
-        float mb = -FLT_MAX;
+        // (4 independent max chains: a single fmax chain over 128 keys is latency-bound)
+        float mx[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
 #pragma unroll 1
-        for (int c0 = 0; c0 < PBK; c0 += 32) {
-          uint32_t s[32];
-          tmem_ld_32x32b_x32(t_s + c0, s);
+        for (int c0 = 0; c0 < PBK; c0 += 64) {
+          uint32_t s0[32], s1[32];
+          tmem_ld_32x32b_x32(t_s + c0, s0);
+          tmem_ld_32x32b_x32(t_s + c0 + 32, s1);
           tmem_ld_wait();
           if (diag) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) mb = fmaxf(mb, c0 + c <= kmax ? __uint_as_float(s[c]) : -FLT_MAX);
+            for (int c = 0; c < 32; ++c) {
+              mx[c & 1] = fmaxf(mx[c & 1], c0 + c <= kmax ? __uint_as_float(s0[c]) : -FLT_MAX);
+              mx[2 + (c & 1)] = fmaxf(mx[2 + (c & 1)], c0 + 32 + c <= kmax ? __uint_as_float(s1[c]) : -FLT_MAX);
+            }
           } else {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) mb = fmaxf(mb, __uint_as_float(s[c]));
+            for (int c = 0; c < 32; ++c) {
+              mx[c & 1] = fmaxf(mx[c & 1], __uint_as_float(s0[c]));
+              mx[2 + (c & 1)] = fmaxf(mx[2 + (c & 1)], __uint_as_float(s1[c]));
+            }
           }
         }
+        float mb = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         mb *= scale_log2;
         const bool grow = mb > m_ref + RESCALE_TH || m_ref == -FLT_MAX;
         float corr = 1.f;
@@ -514,30 +589,17 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
             tmem_st_32x32b_x32(t_o + c, o);
           }
         }
-        // pass 2: P = exp2(s * scale - m) as packed bf16 over S's first 64 columns (the 64
-        // columns of keys [64h, 64h + 64) are read before P's columns [32h, 32h + 32) are written)
-        const float neg = -m_ref;
-#pragma unroll 1
-        for (int h = 0; h < PBK / 64; ++h) {
-          uint32_t s0[32], s1[32], pk[32];
-          tmem_ld_32x32b_x32(t_s + h * 64, s0);
-          tmem_ld_32x32b_x32(t_s + h * 64 + 32, s1);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const uint32_t* src2 = e < 16 ? s0 : s1;
-            const int c = h * 64 + 2 * e;
-            float a = ex2_approx(fmaf(__uint_as_float(src2[(2 * e) & 31]), scale_log2, neg));
-            float b = ex2_approx(fmaf(__uint_as_float(src2[(2 * e + 1) & 31]), scale_log2, neg));
-            if (diag) {
-              a = c <= kmax ? a : 0.f;
-              b = c + 1 <= kmax ? b : 0.f;
-            }
-            l_sum += a + b;
-            pk[e] = pack_bf16x2(a, b);
-          }
-          tmem_st_32x32b_x32(t_s + h * 32, pk);
+        // pass 2: P = exp2(s * scale - m) as packed bf16 over S's first 64 columns
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float2 sc2 = make_float2(scale_log2, scale_log2), ng2 = make_float2(-m_ref, -m_ref);
+        if (diag) {
+          softmax_p_half<true>(t_s, 0, sc2, ng2, kmax, acc);
+          softmax_p_half<true>(t_s, 1, sc2, ng2, kmax, acc);
+        } else {
+          softmax_p_half<false>(t_s, 0, sc2, ng2, kmax, acc);
+          softmax_p_half<false>(t_s, 1, sc2, ng2, kmax, acc);
         }
+        l_sum += (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&sm.p_full[t]);
