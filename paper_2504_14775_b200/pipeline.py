@@ -94,21 +94,46 @@ class MetaChannel:
 
 
 class NcclTransport:
-    """Device-to-device P2P on the default (NCCL) process group, issued on `stream`."""
+    """Device-to-device P2P over NVLink, one NCCL communicator per directed link.
+
+    `links[(src, dst)]` is a two-rank NCCL group. Separate communicators matter: NCCL runs
+    each communicator's operations in order on its own stream, so on a single shared
+    communicator rank 0's send of batch i+1's activations would queue behind its receive of
+    batch i's sampled ids, which completes only after batch i has left the last stage --
+    serialising the pipeline. With one communicator per link (and a distinct one for the
+    token return path, even at PP=2) every hop progresses independently.
+    """
+
+    def __init__(self, rank: int, links: dict):
+        self.rank = rank
+        self.links = links
 
     def send(self, tensor, dst: int, stream) -> None:
         import torch
         import torch.distributed as dist
 
-        with torch.cuda.stream(stream):
-            dist.send(tensor, dst=dst)
+        with torch.cuda.stream(stream) if stream is not None else _null():
+            dist.send(tensor, dst=dst, group=self.links[(self.rank, dst)])
 
     def recv(self, tensor, src: int, stream) -> None:
         import torch
         import torch.distributed as dist
 
-        with torch.cuda.stream(stream):
-            dist.recv(tensor, src=src)
+        with torch.cuda.stream(stream) if stream is not None else _null():
+            dist.recv(tensor, src=src, group=self.links[(src, self.rank)])
+
+
+def make_links(world: int, backend: str = "nccl") -> dict:
+    """Two-rank groups for stage s -> s+1 and for last -> 0 (collective: every rank calls it;
+    `backend="gloo"` gives the CPU tests the same routing)."""
+    import torch.distributed as dist
+
+    links = {}
+    for s in range(world - 1):
+        links[(s, s + 1)] = dist.new_group([s, s + 1], backend=backend)
+    if world > 1:
+        links[(world - 1, 0)] = dist.new_group([0, world - 1], backend=backend)
+    return links
 
 
 class HostTransport:
@@ -446,7 +471,7 @@ def bench_pipeline(args) -> int:
     dist.all_reduce(num_pages, op=dist.ReduceOp.MIN, group=gloo)   # one shared page table: same pool size
     num_pages = int(num_pages.item())
     meta = MetaChannel(gloo, world)
-    transport = HostTransport(gloo) if host_transport else NcclTransport()
+    transport = HostTransport(gloo) if host_transport else NcclTransport(rank, make_links(world))
     from . import native
     launches0 = native.launch_count()
     dist.barrier(group=gloo)

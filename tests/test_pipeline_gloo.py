@@ -82,15 +82,18 @@ def _requests():
     return [RequestSpec(i, float(i) * 0.3, int(rng.integers(5, 60)), int(rng.integers(1, 8))) for i in range(12)]
 
 
-def _run(rank, world, port, q):
+def _run(rank, world, port, q, transport="host"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2504_14775_b200.pipeline import HostTransport, MetaChannel, PipelineExecutor, worker_loop
+    from paper_2504_14775_b200.pipeline import (HostTransport, MetaChannel, NcclTransport, PipelineExecutor,
+                                                make_links, worker_loop)
     from paper_2504_14775_b200.serving import ServingEngine
     reqs = _requests()
     g = dist.group.WORLD
     meta = MetaChannel(g, world)
-    tr = HostTransport(g)
+    # "links": the product transport's per-link group routing (one two-rank group per hop and
+    # one for the token return path), on gloo groups with CPU tensors
+    tr = HostTransport(g) if transport == "host" else NcclTransport(rank, make_links(world, backend="gloo"))
     pages = 64
     try:
         if rank == 0:
@@ -124,12 +127,12 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_pipeline_end_to_end_gloo(world):
+@pytest.mark.parametrize("world,transport", [(2, "host"), (3, "host"), (2, "links"), (3, "links")])
+def test_pipeline_end_to_end_gloo(world, transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     msgs = [q.get(timeout=120) for _ in range(world)]
