@@ -53,6 +53,27 @@ def test_gemm_tcgen05(lib, M, N, K):
     assert _rel(C_, ref + bias.float() + res.float()) < 8e-3
 
 
+@pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096)])
+def test_gemm_deterministic(lib, M, N, K):
+    """Auto tiling (incl. split-K partial sums) is bit-stable across runs and agrees with whole-tile
+    (force_splits=1) tiling to fp32 rounding."""
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    ws = torch.empty(160 << 20, dtype=torch.uint8, device="cuda")
+    outs = []
+    for splits in (0, 0, 0, 1):
+        C_ = torch.full((M, N), float("nan"), device="cuda").bfloat16()
+        lib.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C_.data_ptr(), N, M, N, K, None, res.data_ptr(),
+                 N, 0, splits, ws.data_ptr(), ws.numel(), lib.stream_handle())
+        outs.append(C_)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = A.float() @ B.float().T + res.float()
+    assert _rel(outs[0], ref) < 8e-3 and _rel(outs[3], ref) < 8e-3
+
+
 @pytest.mark.parametrize("M,d_ff,K", [(1, 768, 256), (37, 14336, 4096), (300, 768, 256), (2048, 14336, 4096)])
 def test_gemm_swiglu_fused(lib, M, d_ff, K):
     from paper_2504_14775_b200.modelspec import interleave_gate_up
@@ -95,7 +116,8 @@ def test_gemm_qkv_rope_fused_matches_unfused(lib, M, name, splits):
     # unfused reference path
     ref = torch.empty(M, Q, device="cuda").bfloat16()
     lib.call("gllm_gemm_bf16", A.data_ptr(), d, W.data_ptr(), d, ref.data_ptr(), Q, M, Q, d,
-             None if bias is None else bias.data_ptr(), None, 0, 0, 0, ws.data_ptr(), ws.numel(), st)
+             None if bias is None else bias.data_ptr(), None, 0, 0, 1 if splits == 1 else 0, ws.data_ptr(),
+             ws.numel(), st)
     kr = torch.zeros(512, KV, ps, 128, device="cuda").bfloat16()
     vr = torch.zeros_like(kr)
     lib.call("gllm_rope_kv_write", ref.data_ptr(), M, H, KV, 128, pos.data_ptr(), slot.data_ptr(), rope.data_ptr(),
