@@ -13,6 +13,8 @@
 // Rows past M are zero-filled by TMA on load and masked on store, so decode
 // micro-batches (M = a few tokens) reuse the same kernel; they are HBM-bound on
 // the weight stream, and split-K spreads that stream over all 148 SMs.
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -200,18 +202,29 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
   }
 }
 
-// Persistent: one CTA per SM walks work units u = blockIdx.x, +gridDim.x, ... where a unit is
-// (m-tile, n-tile, K-split) with the m-tile fastest, so the CTAs running at the same time share
-// each weight (B) tile through L2 and the weight matrix streams from HBM ~once per GEMM.
+// Persistent: one CTA (CG = 1) or one CTA pair (CG = 2, a 2-CTA cluster on one TPC) per SM / SM
+// pair walks work units u = cluster id, +#clusters, ... where a unit is (m-tile, n-tile, K-split)
+// with the m-tile fastest, so the CTAs running at the same time share each weight (B) tile
+// through L2 and the weight matrix streams from HBM ~once per GEMM.
+//
+// CG = 2 (tcgen05 cta_group::2): a unit is a 256 x BN tile. Each CTA of the pair TMA-loads its
+// own 128 A rows and HALF of the B tile (BN/2 rows) into its smem; the leader CTA issues
+// M=256 MMAs that read A and B from both CTAs' smem and accumulate each CTA's 128 rows in that
+// CTA's TMEM. Per SM and K-block that is 16 KB (A) + BN/2 x 128 B (B) instead of 16 KB + BN x
+// 128 B: at BN = 256 a third less smem/L2 traffic per MMA, which is what keeps the tensor pipe
+// fed (the 1-CTA kernel is smem-bandwidth bound at ~2/3 of MMA peak). Both CTAs' TMA loads
+// complete on the leader's `full` barrier; the leader's commits multicast `empty` / `acc_full`
+// to both CTAs; both CTAs' epilogue warps arrive on the leader's `acc_empty`.
 // The accumulator is double-buffered in TMEM (2 x BN columns): the epilogue of unit i overlaps
 // the MMAs of unit i+1; the smem ring's phases continue across units.
-template <int BN, int STAGES, int MODE>
+template <int BN, int STAGES, int MODE, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   int M, int N, int K, int k_blocks_per_split, int n_splits, bf16* __restrict__ C, int ldc,
                   const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
                   float* __restrict__ partial, const QkvRopeArgs qa) {
-  using L = GemmSmem<BN, STAGES>;
+  static_assert(CG == 1 || CG == 2, "cta_group 1 or 2");
+  using L = GemmSmem<BN / CG, STAGES>;   // per-CTA stage: 128 A rows + BN/CG B rows
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * L::STAGE_BYTES);
@@ -222,10 +235,13 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_tiles = (M + BM - 1) / BM;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  constexpr int TM = BM * CG;           // rows per unit
+  const int m_tiles = (M + TM - 1) / TM;
   const int n_tiles = N / BN;
   const int units = m_tiles * n_tiles * n_splits;
   const int total_kb = K / BK;
+  const int unit0 = blockIdx.x / CG, ustride = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -236,13 +252,14 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);   // one arrival per epilogue warp
+      mbar_init(&acc_empty[a], 4 * CG);   // one arrival per epilogue warp of every CTA
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, 2 * BN);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -251,7 +268,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
     const int rest = u / m_tiles;
     const int nt = rest % n_tiles;
     split = rest / n_tiles;
-    m0 = mt * BM;
+    m0 = mt * TM;
     n0 = nt * BN;
     kb0 = split * k_blocks_per_split;
     nkb = min(total_kb, kb0 + k_blocks_per_split) - kb0;
@@ -260,75 +277,92 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
   if (warp == 0) {
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream through once per step
+      // both CTAs' loads complete on the leader's `full` barrier (CG = 2)
+      const uint32_t full_leader = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
       int it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = unit0; u < units; u += ustride) {
         int m0, n0, split, kb0, nkb;
         unit_coords(u, m0, n0, split, kb0, nkb);
+        const int am = m0 + (int)rank * BM, bn = n0 + (int)rank * (BN / CG);
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
-          mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
           const int kc = (kb0 + i) * BK;
-          tma_load_2d(&map_a, &full[s], sa, kc, m0);
-          tma_load_2d_hint(&map_b, &full[s], sb, kc, n0, pol_w);
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+            tma_load_2d(&map_a, &full[s], sa, kc, am);
+            tma_load_2d_hint(&map_b, &full[s], sb, kc, bn, pol_w);
+          } else {
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+            const uint32_t bar = full_leader + (uint32_t)(s * 8);
+            tma_load_2d_cg2(&map_a, bar, sa, kc, am, policy_evict_last());
+            tma_load_2d_cg2(&map_b, bar, sb, kc, bn, pol_w);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-    int it = 0, lt = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
-      int m0, n0, split, kb0, nkb;
-      unit_coords(u, m0, n0, split, kb0, nkb);
-      const int acc = lt & 1;
-      mbar_wait(&acc_empty[acc], ((lt >> 1) & 1) ^ 1);   // epilogue drained this buffer
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-      for (int i = 0; i < nkb; ++i, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+    if (CG == 1 || rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(TM, BN);
+      int it = 0, lt = 0;
+      for (int u = unit0; u < units; u += ustride, ++lt) {
+        int m0, n0, split, kb0, nkb;
+        unit_coords(u, m0, n0, split, kb0, nkb);
+        const int acc = lt & 1;
+        mbar_wait(&acc_empty[acc], ((lt >> 1) & 1) ^ 1);   // every epilogue drained this buffer
         tc_fence_after();
-        if (elect_one()) {
-          const uint8_t* sa = smem + s * L::STAGE_BYTES;
-          const uint8_t* sb = sa + L::A_BYTES;
-          const uint64_t da = smem_desc_sw128(sa);
-          const uint64_t db = smem_desc_sw128(sb);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint8_t* sa = smem + s * L::STAGE_BYTES;
+            const uint8_t* sb = sa + L::A_BYTES;
+            const uint64_t da = smem_desc_sw128(sa);
+            const uint64_t db = smem_desc_sw128(sb);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // +32 B along K inside the swizzle atom = +2 in the 16-byte address field.
-            mma_bf16_ss(d_tmem, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              // +32 B along K inside the swizzle atom = +2 in the 16-byte address field.
+              mma_bf16_ss_cg<CG>(d_tmem, da + 2 * k, db + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit_cg<CG>(&empty[s]);
+            if (i == nkb - 1) mma_commit_cg<CG>(&acc_full[acc]);
           }
-          mma_commit(&empty[s]);
-          if (i == nkb - 1) mma_commit(&acc_full[acc]);
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else {
     // Epilogue warps 2-5: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
     const int q = warp & 3;
+    const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(acc_empty), 0) : 0u;
     int lt = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++lt) {
+    for (int u = unit0; u < units; u += ustride, ++lt) {
       int m0, n0, split, kb0, nkb;
       unit_coords(u, m0, n0, split, kb0, nkb);
       const int acc = lt & 1;
       mbar_wait(&acc_full[acc], (lt >> 1) & 1);
       tc_fence_after();
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      epilogue_tile<BN, MODE>(lane_base, m0 + q * 32 + lane, n0, split, M, N, C, ldc, bias, residual, ldr, partial,
-                              qa);
+      epilogue_tile<BN, MODE>(lane_base, m0 + (int)rank * BM + q * 32 + lane, n0, split, M, N, C, ldc, bias,
+                              residual, ldr, partial, qa);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&acc_empty[acc]);
+        else mbar_arrive_cluster(acc_empty_leader + (uint32_t)(acc * 8));
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, 2 * BN);
+  if constexpr (CG == 2) cluster_sync();  // the peer's MMAs / remote arrivals are done
+  if (warp == 1) tmem_dealloc_cg<CG>(tmem_base, 2 * BN);
 }
 
 // Sum split-K partials [splits, M, N] fp32 and apply the epilogue; 8 columns per thread.
@@ -477,22 +511,39 @@ int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t col
   return make_map(out, ptr, rows, cols, ld, box_rows);
 }
 
-template <int BN, int STAGES, int MODE>
+template <int BN, int STAGES, int MODE, int CG = 1>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits, int kbps,
                        bf16* C, int ldc, const bf16* bias, const bf16* res, int ldr, float* partial,
                        cudaStream_t st, const QkvRopeArgs& qa = QkvRopeArgs{}) {
-  constexpr int smem = GemmSmem<BN, STAGES>::TOTAL;
+  constexpr int smem = GemmSmem<BN / CG, STAGES>::TOTAL;
+  auto kern = gemm_bf16_tcgen05<BN, STAGES, MODE, CG>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05<BN, STAGES, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     attr_done = true;
   }
-  const long units = (long)((M + BM - 1) / BM) * (N / BN) * splits;
-  const int grid = (int)(units < device_sm_count() ? units : device_sm_count());
-  gemm_bf16_tcgen05<BN, STAGES, MODE><<<grid, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, splits, C, ldc, bias,
-                                                                        res, ldr, partial, qa);
+  const long units = (long)((M + BM * CG - 1) / (BM * CG)) * (N / BN) * splits;
+  const long slots = device_sm_count() / CG;
+  const int clusters = (int)(units < slots ? units : slots);
+  if constexpr (CG == 1) {
+    kern<<<clusters, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, splits, C, ldc, bias, res, ldr, partial, qa);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, kbps, splits, C, ldc, bias, res, ldr, partial, qa);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm 2-CTA launch");
+  }
   return check_launch("gemm_bf16_tcgen05");
 }
 
@@ -537,10 +588,17 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       return set_error(GLLM_ERR_INVALID, "gemm split-K workspace too small (%zu < %zu)", ws_bytes, need);
     partial = reinterpret_cast<float*>(workspace);
   }
+  // 2-CTA (cta_group::2) tiles once there is more than one 128-row tile and no split-K; decode
+  // micro-batches (M <= 128) stay on the 1-CTA kernel. GLLM_GEMM_CG=1 forces 1-CTA (A/B runs).
+  static const int cg_pref = [] {
+    const char* e = getenv("GLLM_GEMM_CG");
+    return e ? atoi(e) : 2;
+  }();
+  const int cg = (cg_pref == 2 && splits == 1 && m_tiles >= 2 && bn >= 128) ? 2 : 1;
   CUtensorMap ma, mb;
   const int a_rows = a_rows_alloc > M ? a_rows_alloc : M;
   if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;
-  if (int rc = make_map(&mb, B, N, K, ldb, bn)) return rc;
+  if (int rc = make_map(&mb, B, N, K, ldb, bn / cg)) return rc;
   int rc = 0;
   if (qkv && splits > 1) {
     // small-M QKV: split-K plain GEMM, then the standalone RoPE + KV-write kernel
@@ -566,6 +624,22 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       rc = launch_gemm<BNV, ST, EPI_QKV_ROPE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, nullptr, 0,       \
                                               nullptr, st, *qkv);                                            \
   }
+#define GLLM_GEMM_CASE2(BNV, ST)                                                                              \
+  if (bn == BNV) {                                                                                            \
+    if (mode == EPI_STORE)                                                                                    \
+      rc = launch_gemm<BNV, ST, EPI_STORE, 2>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual, ldr,     \
+                                              nullptr, st);                                                   \
+    else if (mode == EPI_SWIGLU)                                                                              \
+      rc = launch_gemm<BNV, ST, EPI_SWIGLU, 2>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0,    \
+                                               nullptr, st);                                                  \
+    else                                                                                                      \
+      rc = launch_gemm<BNV, ST, EPI_QKV_ROPE, 2>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, nullptr, 0,     \
+                                                 nullptr, st, *qkv);                                          \
+  }
+  if (cg == 2) {
+    GLLM_GEMM_CASE2(256, 6)
+    else GLLM_GEMM_CASE2(128, 8) else return set_error(GLLM_ERR_INVALID, "bad BN %d for 2-CTA tiles", bn);
+  } else
   GLLM_GEMM_CASE(256, 4)
   else GLLM_GEMM_CASE(128, 6) else if (bn == 64 && !swiglu && !qkv) {
     rc = mode == EPI_STORE ? launch_gemm<64, 8, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual,
@@ -574,6 +648,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
                                                                  nullptr, 0, partial, st);
   } else return set_error(GLLM_ERR_INVALID, "bad BN %d (swiglu/qkv need >= 128)", bn);
 #undef GLLM_GEMM_CASE
+#undef GLLM_GEMM_CASE2
   if (rc) return rc;
   if (splits > 1) {
     const int threads = 256;
