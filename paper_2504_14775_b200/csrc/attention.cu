@@ -44,7 +44,7 @@ constexpr int NWARP = ATT_THREADS / 32;
 constexpr int PM = 128;          // query rows per tile (MMA M = TMEM lanes)
 constexpr int PTILES = 2;        // query tiles per CTA, ping-ponged on the tensor core
 constexpr int PBK = 128;         // keys per block (MMA N of S, MMA K of P.V)
-constexpr int PRING = 4;         // K/V block ring: K_j, V_j, K_j+1, V_j+1
+constexpr int PRING = 5;         // K/V block ring (K_j, V_j, K_j+1, ...): 2.5 blocks of prefetch
 constexpr int PF_THREADS = 320;  // warps 0-7 softmax (tile = warp / 4), warp 8 TMA, warp 9 MMA
 constexpr int PF_TMEM_COLS = 512;
 constexpr float RESCALE_TH = 8.f;
@@ -440,6 +440,7 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       const int n_pages = (kv_len + page_size - 1) / page_size;
       const int ppb = PBK / page_size;
       const uint32_t box_bytes = (uint32_t)page_size * 128;
+      const uint64_t pol = policy_evict_last();  // every query tile of the sequence re-reads these pages
       for (int f = 0; f < 2 * nb; ++f) {
         const int s = f % PRING;
         if (f >= PRING) mbar_wait(&sm.kv_empty[s], ((f / PRING) + 1) & 1);
@@ -450,8 +451,8 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
           // pages past the item's last key repeat its last page (never an unmapped table entry)
           const int p = min(j * ppb + pl, n_pages - 1);
           const int row0 = (table[p] * n_kv + kvh) * page_size;
-          tma_load_2d(m, &sm.kv_full[s], sm.kv[s][0] + pl * box_bytes, 0, row0);
-          tma_load_2d(m, &sm.kv_full[s], sm.kv[s][1] + pl * box_bytes, 64, row0);
+          tma_load_2d_hint(m, &sm.kv_full[s], sm.kv[s][0] + pl * box_bytes, 0, row0, pol);
+          tma_load_2d_hint(m, &sm.kv_full[s], sm.kv[s][1] + pl * box_bytes, 64, row0, pol);
         }
       }
     }
