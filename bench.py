@@ -139,16 +139,18 @@ def roofline(profile: dict, peaks: dict) -> dict:
         achieved = e["bytes"] / e["launches"] / (per_launch_ms * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
         out = {"bound": "hbm", "unit": "GB/s", "algorithmic_per_launch": e["bytes"] / e["launches"]}
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # DRAM bytes per launch of this kernel class from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             t = json.load(fh).get(name)
         if t:
-            traffic = {"bytes_per_launch": t["dram_bytes_per_launch"], "shape": t["shape"]}
+            traffic = t["dram_bytes_per_launch"]
+            traffic_src = f"profiles/ncu_traffic.json ({t['shape']})"
     except OSError:
         pass
     out.update({"kernel": name, "achieved": round(achieved, 2), "peak": peak, "frac": round(achieved / peak, 4),
-                "traffic": traffic, "launches": e["launches"], "avg_launch_ms": round(per_launch_ms, 4),
+                "traffic": traffic, "traffic_src": traffic_src, "launches": e["launches"],
+                "avg_launch_ms": round(per_launch_ms, 4),
                 "peak_src": peaks["src"] + (" sustained" if out["bound"] == "tensor" else "")})
     return out
 
