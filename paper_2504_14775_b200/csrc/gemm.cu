@@ -37,15 +37,6 @@ struct GemmSmem {
 
 enum : int { EPI_STORE = 0, EPI_PARTIAL_F32 = 1, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3 };
 
-// Extra epilogue operands of EPI_QKV_ROPE (RoPE on q/k + paged KV-cache write).
-struct QkvRopeArgs {
-  const int* tok_pos;    // [M] absolute position of each token row
-  const int* tok_slot;   // [M] paged slot: page * page_size + offset
-  const float* rope;     // [max_pos][64][2] (cos, sin)
-  bf16* k_cache;         // this layer's [pages][n_kv][page_size][128]
-  bf16* v_cache;
-  int n_heads, n_kv, page_size;
-};
 
 // Epilogue of one 128 x BN output tile held in TMEM columns [acc_col, acc_col + BN):
 // warp (w % 4) reads TMEM lanes [32q, 32q+32), i.e. output rows m0 + 32q + lane.
@@ -555,6 +546,11 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
                      const QkvRopeArgs* qkv = nullptr) {
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return set_error(GLLM_ERR_INVALID, "gemm needs K %% 64 == 0 and N %% 64 == 0 (K=%d N=%d)", K, N);
+  // decode-sized M: swap-AB stream-K weight streaming (gemm_skinny.cu)
+  if (force_splits == 0 && force_bn == 0 && gemm_skinny_eligible(M, N, K) &&
+      ws_bytes >= gemm_skinny_workspace_bytes(M, N, K) && !(swiglu && (bias || residual)))
+    return gemm_skinny(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, swiglu ? EPI_SWIGLU : (qkv ? EPI_QKV_ROPE : EPI_STORE),
+                       bias, residual, ldr, qkv, workspace, ws_bytes, st);
   if (ldc % 8 || (residual && ldr % 8)) return set_error(GLLM_ERR_INVALID, "gemm output pitch must be a multiple of 8");
   if (swiglu && (N % 128 || bias || residual)) return set_error(GLLM_ERR_INVALID, "swiglu gemm needs N %% 128 == 0, no bias/residual");
   const int num_sms = device_sm_count();

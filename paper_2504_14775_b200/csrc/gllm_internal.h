@@ -17,6 +17,16 @@ int set_cuda_error(cudaError_t e, const char* what);
 int check_launch(const char* what);
 int device_sm_count();
 
+// Extra epilogue operands of the fused QKV GEMM (RoPE on q/k + paged KV-cache write).
+struct QkvRopeArgs {
+  const int* tok_pos;    // [M] absolute position of each token row
+  const int* tok_slot;   // [M] paged slot: page * page_size + offset
+  const float* rope;     // [max_pos][64][2] (cos, sin)
+  bf16* k_cache;         // this layer's [pages][n_kv][page_size][128]
+  bf16* v_cache;
+  int n_heads, n_kv, page_size;
+};
+
 // gemm.cu
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K, const bf16* bias,
               const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits, void* workspace,
@@ -32,6 +42,17 @@ int gemm_qkv_rope_bf16(const bf16* A, int lda, const bf16* W, int ldb, const bf1
                        bf16* k_cache, bf16* v_cache, int page_size, int a_rows_alloc, int force_bn,
                        int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st);
 size_t gemm_workspace_bytes(int M, int N, int K);
+
+// gemm_skinny.cu: M <= 32 (decode) GEMMs; mode 0 store (+bias/+residual), 2 SwiGLU, 3 QKV+RoPE+KV write.
+// The workspace head holds tile counters that must be zero at launch: the stage zeroes them once
+// per forward (gemm_ws_reset) and every launch leaves them zero; other callers get a memset per call.
+bool gemm_skinny_eligible(int M, int N, int K);
+size_t gemm_skinny_workspace_bytes(int M, int N, int K);
+int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,
+                int K, int mode, const bf16* bias, const bf16* residual, int ldr, const QkvRopeArgs* qkv,
+                void* workspace, size_t ws_bytes, cudaStream_t st);
+int gemm_ws_reset(void* workspace, cudaStream_t st);
+void gemm_ws_mark_clean(const void* workspace);
 // bf16 [rows, cols] (leading dim ld) as a TMA map with 64-col x box_rows boxes, 128B swizzle (cached)
 int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 

@@ -216,6 +216,11 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
   MetaView mv = meta_view(B);
   bf16* x = B.hidden ? reinterpret_cast<bf16*>(B.hidden) : w.x;
   const int maxT = d.max_tokens;
+  // skinny-GEMM tile counters zeroed once per forward; every GEMM leaves them zero again
+  struct CleanGuard {
+    ~CleanGuard() { gemm_ws_mark_clean(nullptr); }
+  } clean_guard;
+  if (int rc = gemm_ws_reset(w.gemm, st)) return rc;
 
   // Algorithmic attention work of this batch (profiler only; needs the host seq_info copy).
   double att_flops = 0, att_bytes = 0;
