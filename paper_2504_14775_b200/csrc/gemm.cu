@@ -579,10 +579,11 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   splits = (total_kb + kbps - 1) / kbps;
   float* partial = nullptr;
   if (splits > 1) {
-    size_t need = (size_t)splits * M * N * sizeof(float);
+    // split-K partials live after the skinny kernel's tile counters (which must stay zero)
+    size_t need = GEMM_WS_HEAD_BYTES + (size_t)splits * M * N * sizeof(float);
     if (workspace == nullptr || ws_bytes < need)
       return set_error(GLLM_ERR_INVALID, "gemm split-K workspace too small (%zu < %zu)", ws_bytes, need);
-    partial = reinterpret_cast<float*>(workspace);
+    partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + GEMM_WS_HEAD_BYTES);
   }
   // 2-CTA (cta_group::2) tiles once there is more than one 128-row tile and no split-K; decode
   // micro-batches (M <= 128) stay on the 1-CTA kernel. GLLM_GEMM_CG=1 forces 1-CTA (A/B runs).

@@ -334,7 +334,7 @@ thread_local const void* t_clean_ws = nullptr;
 
 }  // namespace
 
-constexpr size_t SKINNY_COUNTER_BYTES = 16384;
+constexpr size_t SKINNY_COUNTER_BYTES = GEMM_WS_HEAD_BYTES;
 
 void gemm_ws_mark_clean(const void* workspace) { t_clean_ws = workspace; }
 

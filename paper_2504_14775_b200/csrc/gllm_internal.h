@@ -46,6 +46,7 @@ size_t gemm_workspace_bytes(int M, int N, int K);
 // gemm_skinny.cu: M <= 32 (decode) GEMMs; mode 0 store (+bias/+residual), 2 SwiGLU, 3 QKV+RoPE+KV write.
 // The workspace head holds tile counters that must be zero at launch: the stage zeroes them once
 // per forward (gemm_ws_reset) and every launch leaves them zero; other callers get a memset per call.
+constexpr size_t GEMM_WS_HEAD_BYTES = 16384;  // skinny tile counters at the head of every GEMM workspace
 bool gemm_skinny_eligible(int M, int N, int K);
 size_t gemm_skinny_workspace_bytes(int M, int N, int K);
 int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,

@@ -163,7 +163,7 @@ static StageWs carve(const gllm_dims& d, uint8_t* base) {
   w.tok_id = (int*)take(T * 4);
   w.emit_rows = (int*)take(E * 4);
   // split-K partials: splits * tiles <= 2 * SMs, tile <= 128 x 256 fp32
-  w.gemm_bytes = (size_t)2 * 160 * 128 * 256 * 4;
+  w.gemm_bytes = 16384 + (size_t)2 * 160 * 128 * 256 * 4;
   w.gemm = (float*)take(w.gemm_bytes);
   w.total = off;
   return w;

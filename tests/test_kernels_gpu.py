@@ -53,6 +53,34 @@ def test_gemm_tcgen05(lib, M, N, K):
     assert _rel(C_, ref + bias.float() + res.float()) < 8e-3
 
 
+@pytest.mark.parametrize("M,N,K", [(4, 5120, 5120), (1, 32000, 256), (16, 4096, 14336), (32, 6144, 4096),
+                                   (7, 256, 768)])
+def test_gemm_skinny_stream_k(lib, M, N, K):
+    """Decode-sized GEMMs (swap-AB stream-K: tiles shared by CTAs fixed up by the last arriver) vs
+    fp32, with bias + residual, after a split-K GEMM has used the same workspace (its partials
+    must not clobber the tile counters), and bit-stable across runs."""
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    ws = torch.empty(160 << 20, dtype=torch.uint8, device="cuda")
+    A2 = torch.randn(100, K, device="cuda", generator=g).bfloat16()
+    junk = torch.empty(100, N, device="cuda").bfloat16()
+    ref = A.float() @ B.float().T + bias.float() + res.float()
+    outs = []
+    for _ in range(2):
+        lib.call("gllm_gemm_bf16", A2.data_ptr(), K, B.data_ptr(), K, junk.data_ptr(), N, 100, N, K, None, None, 0,
+                 0, 3, ws.data_ptr(), ws.numel(), lib.stream_handle())            # split-K on the same workspace
+        C_ = torch.full((M, N), float("nan"), device="cuda").bfloat16()
+        lib.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C_.data_ptr(), N, M, N, K, bias.data_ptr(),
+                 res.data_ptr(), N, 0, 0, ws.data_ptr(), ws.numel(), lib.stream_handle())
+        outs.append(C_)
+    torch.cuda.synchronize()
+    assert _rel(outs[0], ref) < 8e-3, _rel(outs[0], ref)
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096)])
 def test_gemm_deterministic(lib, M, N, K):
     """Auto tiling (incl. split-K partial sums) is bit-stable across runs and agrees with whole-tile
