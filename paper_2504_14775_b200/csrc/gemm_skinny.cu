@@ -25,11 +25,11 @@ namespace {
 constexpr int W_ROWS = 128;  // output features per tile (MMA M)
 constexpr int KB = 64;       // K per stage (one 128-byte swizzle atom of bf16)
 constexpr int THREADS = 192;
-constexpr int STAGES = 8;
 constexpr int EPI_STORE = 0, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3;
 
 template <int NT>
 struct SkSmem {
+  static constexpr int STAGES = 8;
   static constexpr int W_BYTES = W_ROWS * KB * 2;
   static constexpr int X_BYTES = NT * KB * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
@@ -158,6 +158,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
                     const bf16* __restrict__ residual, int ldr, float* __restrict__ partial,
                     int* __restrict__ counters, const QkvRopeArgs qa) {
   using L = SkSmem<NT>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* st = reinterpret_cast<float*>(smem + L::EPI_OFF);
@@ -248,15 +249,20 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
       tc_fence_after();
       float v[NT];
       {
-        uint32_t r[NT];
         const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NT);
-        if constexpr (NT == 32)
-          tmem_ld_32x32b_x32(ta, r);
-        else
+        if constexpr (NT == 16) {
+          uint32_t r[16];
           tmem_ld_32x32b_x16(ta, r);
-        tmem_ld_wait();
+          tmem_ld_wait();
 #pragma unroll
-        for (int m = 0; m < NT; ++m) v[m] = __uint_as_float(r[m]);
+          for (int m = 0; m < 16; ++m) v[m] = __uint_as_float(r[m]);
+        } else {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(ta, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int m = 0; m < 32; ++m) v[m] = __uint_as_float(r[m]);
+        }
       }
       tc_fence_before();
       __syncwarp();

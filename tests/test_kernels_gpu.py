@@ -53,7 +53,7 @@ def test_gemm_tcgen05(lib, M, N, K):
     assert _rel(C_, ref + bias.float() + res.float()) < 8e-3
 
 
-@pytest.mark.parametrize("M,N,K", [(4, 5120, 5120), (1, 32000, 256), (16, 4096, 14336), (32, 6144, 4096),
+@pytest.mark.parametrize("M,N,K", [(4, 5120, 5120), (1, 32000, 256), (16, 4096, 14336), (32, 6144, 4096), (31, 5120, 5120),
                                    (7, 256, 768)])
 def test_gemm_skinny_stream_k(lib, M, N, K):
     """Decode-sized GEMMs (swap-AB stream-K: tiles shared by CTAs fixed up by the last arriver) vs
