@@ -141,7 +141,14 @@ GLLM_API int gllm_stage_forward(const gllm_stage* stage, const gllm_batch* batch
 GLLM_API int gllm_commit_tokens(const gllm_stage* stage, const gllm_batch* batch, const int32_t* sampled,
                        gllm_stream_t stream);
 
-/* ---- individual kernels (tests, custom stages) ---- */
+/* ---- individual kernels (tests, custom stages) ----
+ * GEMM tiling is chosen per call: M <= 32 -> swap-AB stream-K "skinny" kernel (decode);
+ * more than one 128-row tile and no split -> 2-CTA (cta_group::2) 256 x BN tiles; otherwise
+ * 1-CTA 128 x BN tiles, split-K when one wave is not filled. force_bn / force_splits != 0 pin
+ * the 1-/2-CTA tile path (force_splits = 1: whole tiles, >= 2: split-K). The workspace head
+ * (16 KB) holds tile counters that must be zero between calls; these entry points zero them
+ * themselves (gllm_stage_forward once per forward). workspace >= 16 KB + 42 MB covers every
+ * shape a stage issues. */
 GLLM_API int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N, int K,
                    const void* bias, const void* residual, int ldr, int force_bn, int force_splits,
                    void* workspace, size_t workspace_bytes, gllm_stream_t stream);
