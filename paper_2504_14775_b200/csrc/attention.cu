@@ -382,6 +382,8 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
   PrefillSmem& sm =
       *reinterpret_cast<PrefillSmem*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   constexpr int QT = PM / G;  // query tokens per tile
+  pdl_trigger();
+  pdl_wait();
   const int kvh = blockIdx.x;
   const int item = n_work - 1 - (int)blockIdx.y;  // a chunk's later (longer) tiles start first
   const int sidx = work[2 * item], q0 = work[2 * item + 1];
@@ -644,6 +646,8 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_const
                    float scale_log2, bf16* __restrict__ out) {
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  pdl_trigger();
+  pdl_wait();
   const int kvh = blockIdx.x;   // kv heads fastest: a work item's CTAs launch together
   const int item = blockIdx.y;
   const int sidx = work[2 * item];
@@ -684,8 +688,9 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
                                                             n_heads, n_kv, page_size, scale_log2, out);
     return check_launch("attention_prefill");
   } else {
-    attn_decode_kernel<G><<<grid, ATT_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, block_table, mpr, n_heads,
-                                                           n_kv, page_size, scale_log2, out);
+    cudaError_t e = launch_kernel(attn_decode_kernel<G>, grid, dim3(ATT_THREADS), smem, st, 1, km, vm, qkv, seq_info,
+                                  work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out);
+    if (e != cudaSuccess) return set_cuda_error(e, "attention_decode launch");
     return check_launch("attention_decode");
   }
 }

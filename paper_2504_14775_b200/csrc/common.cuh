@@ -54,6 +54,13 @@ GLLM_DEVICE bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with programmatic stream serialization may start while its predecessor
+// still runs: everything before pdl_wait() must not touch memory the predecessor writes or
+// reads (weights and smem setup only). pdl_trigger() lets the successor launch early.
+GLLM_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+GLLM_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // ---------------------------------------------------------------- mbarrier
 GLLM_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -226,6 +226,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   constexpr int TM = BM * CG;           // rows per unit
   const int m_tiles = (M + TM - 1) / TM;
@@ -267,6 +268,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
 
   if (warp == 0) {
     if (elect_one()) {
+      pdl_wait();  // A is the predecessor's output
       const uint64_t pol_w = policy_evict_first();  // weights stream through once per step
       // both CTAs' loads complete on the leader's `full` barrier (CG = 2)
       const uint32_t full_leader = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
@@ -330,6 +332,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
     }
   } else {
     // Epilogue warps 2-5: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+    pdl_wait();  // C / residual / KV cache are shared with the predecessor
     const int q = warp & 3;
     const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(acc_empty), 0) : 0u;
     int lt = 0;
@@ -517,24 +520,9 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   const long units = (long)((M + BM * CG - 1) / (BM * CG)) * (N / BN) * splits;
   const long slots = device_sm_count() / CG;
   const int clusters = (int)(units < slots ? units : slots);
-  if constexpr (CG == 1) {
-    kern<<<clusters, GEMM_THREADS, smem, st>>>(ma, mb, M, N, K, kbps, splits, C, ldc, bias, res, ldr, partial, qa);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(GEMM_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, kbps, splits, C, ldc, bias, res, ldr, partial, qa);
-    if (e != cudaSuccess) return set_cuda_error(e, "gemm 2-CTA launch");
-  }
+  cudaError_t e = launch_kernel(kern, dim3(CG * clusters), dim3(GEMM_THREADS), smem, st, CG, ma, mb, M, N, K, kbps,
+                                splits, C, ldc, bias, res, ldr, partial, qa);
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return check_launch("gemm_bf16_tcgen05");
 }
 

@@ -170,6 +170,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
   volatile uint32_t* last_flag = tmem_slot + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
   const int kbs = K / KB;
   const int work = (N / W_ROWS) * kbs;
   const int g_begin = blockIdx.x * per, g_end = min(g_begin + per, work);
@@ -197,18 +198,26 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream once per step
       const uint64_t pol_x = policy_evict_last();   // the activations are re-read by every CTA
-      int it = 0;
-      for (int g = g_begin; g < g_end;) {
-        const int t = g / kbs, kb0 = g - t * kbs, nkb = min(kbs - kb0, g_end - g);
-        for (int i = 0; i < nkb; ++i, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-          uint8_t* sw = smem + s * L::STAGE_BYTES;
+      // The CTA's range is contiguous: iteration i is K-block (g_begin + i) % kbs of tile
+      // (g_begin + i) / kbs. The weights of the first STAGES iterations are fetched before the
+      // predecessor kernel has finished (PDL); only the activations wait for it.
+      const int n_it = g_end - g_begin, pre = min(n_it, STAGES);
+      for (int i = 0; i < pre; ++i) {
+        const int g = g_begin + i, t = g / kbs;
+        mbar_arrive_expect_tx(&full[i], L::STAGE_BYTES);
+        tma_load_2d_hint(&map_w, &full[i], smem + i * L::STAGE_BYTES, (g - t * kbs) * KB, t * W_ROWS, pol_w);
+      }
+      pdl_wait();
+      for (int i = 0; i < n_it; ++i) {
+        const int g = g_begin + i, t = g / kbs, kc = (g - t * kbs) * KB;
+        const int s = i % STAGES;
+        uint8_t* sw = smem + s * L::STAGE_BYTES;
+        if (i >= pre) {
+          mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
-          tma_load_2d_hint(&map_w, &full[s], sw, (kb0 + i) * KB, t * W_ROWS, pol_w);
-          tma_load_2d_hint(&map_x, &full[s], sw + L::W_BYTES, (kb0 + i) * KB, 0, pol_x);
+          tma_load_2d_hint(&map_w, &full[s], sw, kc, t * W_ROWS, pol_w);
         }
-        g += nkb;
+        tma_load_2d_hint(&map_x, &full[s], sw + L::W_BYTES, kc, 0, pol_x);
       }
     }
   } else if (warp == 1) {
@@ -239,6 +248,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
     }
   } else {
     // epilogue warps 2-5: warp q = w % 4 reads TMEM lanes [32q, 32q + 32) = W rows of the tile
+    pdl_wait();  // writes C / partials, reads the residual
     const int q = warp & 3, f = q * 32 + lane, et = threadIdx.x - 64;
     int lt = 0;
     for (int g = g_begin; g < g_end; ++lt) {
@@ -331,8 +341,9 @@ int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, in
     if (e != cudaSuccess) return set_cuda_error(e, "skinny gemm smem attribute");
     attr = true;
   }
-  gemm_skinny_tcgen05<NT, MODE><<<grid, THREADS, smem, st>>>(mw, mx, M, N, K, per, C, ldc, bias, res, ldr, partial,
-                                                              counters, qa);
+  cudaError_t e = launch_kernel(gemm_skinny_tcgen05<NT, MODE>, dim3(grid), dim3(THREADS), smem, st, 1, mw, mx, M, N, K,
+                                per, C, ldc, bias, res, ldr, partial, counters, qa);
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm_skinny_tcgen05 launch");
   return check_launch("gemm_skinny_tcgen05");
 }
 

@@ -13,6 +13,38 @@ namespace gllm {
 typedef __nv_bfloat16 bf16;
 
 int set_error(int code, const char* fmt, ...);
+
+// Programmatic dependent launch on (default on; GLLM_PDL=0 turns it off for A/B runs).
+bool pdl_enabled();
+
+// cudaLaunchKernelEx with programmatic stream serialization (when enabled) and an optional
+// cluster: the kernel must call pdl_wait() before touching its predecessor's memory.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster_x,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 int set_cuda_error(cudaError_t e, const char* what);
 int check_launch(const char* what);
 int device_sm_count();

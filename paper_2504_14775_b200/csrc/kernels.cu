@@ -100,6 +100,8 @@ int embed_tokens(const int* tok_id, int n_tokens, const bf16* embed, int d, bf16
 template <int VEC_PER_THREAD>
 __global__ void rmsnorm_kernel(const bf16* __restrict__ x, int ldx, const int* __restrict__ row_index,
                                const bf16* __restrict__ w, bf16* __restrict__ out, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
   const uint4* xp = reinterpret_cast<const uint4*>(x + (size_t)src * ldx);
@@ -160,10 +162,13 @@ int rmsnorm(const bf16* x, int ldx, const int* row_index, const bf16* w, bf16* o
   if (d % 8) return set_error(GLLM_ERR_INVALID, "rmsnorm needs d %% 8 == 0");
   const int nvec = d / 8;
   if (nvec <= 128) {
-    rmsnorm_kernel<1><<<rows, 128, 0, st>>>(x, ldx, row_index, w, out, d, eps);
+    cudaError_t e = launch_kernel(rmsnorm_kernel<1>, dim3(rows), dim3(128), 0, st, 1, x, ldx, row_index, w, out, d, eps);
+    if (e != cudaSuccess) return set_cuda_error(e, "rmsnorm launch");
   } else if (nvec <= 1024) {
     const int threads = ((nvec + 3) / 4 + 31) / 32 * 32;
-    rmsnorm_kernel<4><<<rows, threads, 0, st>>>(x, ldx, row_index, w, out, d, eps);
+    cudaError_t e =
+        launch_kernel(rmsnorm_kernel<4>, dim3(rows), dim3(threads), 0, st, 1, x, ldx, row_index, w, out, d, eps);
+    if (e != cudaSuccess) return set_cuda_error(e, "rmsnorm launch");
   } else {
     return set_error(GLLM_ERR_INVALID, "rmsnorm d=%d too large", d);
   }

@@ -120,6 +120,13 @@ static int check_finite(const bf16* x, size_t n, const char* what, int layer, cu
 static double gemm_bytes(double M, double N, double K, bool residual, bool bias) {
   return 2.0 * (M * K + N * K + M * N) + (residual ? 2.0 * M * N : 0.0) + (bias ? 2.0 * N : 0.0);
 }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GLLM_PDL");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return on;
+}
 int device_sm_count() {
   static int n = 0;
   if (n == 0) {
