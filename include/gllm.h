@@ -178,6 +178,15 @@ GLLM_API int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, con
                           const void* k_cache,
                           const void* v_cache, int n_heads, int n_kv_heads, int head_dim, int page_size, void* out,
                           gllm_stream_t stream);
+/* same, with each prefill item's key range cut into n_split parts (more CTAs when a micro-batch has
+ * few long chunks), merged by a combine pass; workspace >= gllm_attn_split_workspace_bytes(...).
+ * gllm_stage_forward picks n_split itself from the host metadata. */
+GLLM_API int gllm_attn_mixed_paged_split(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
+                                         int n_prefill_work, const int32_t* block_table, int max_pages_per_row,
+                                         int kv_pages, const void* k_cache, const void* v_cache, int n_heads,
+                                         int n_kv_heads, int head_dim, int page_size, void* out, int n_split,
+                                         void* workspace, size_t workspace_bytes, gllm_stream_t stream);
+GLLM_API size_t gllm_attn_split_workspace_bytes(int n_prefill_work, int n_split, int n_kv_heads);
 GLLM_API int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream);
 
 /* ---- measurement ---- */

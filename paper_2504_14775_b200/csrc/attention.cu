@@ -30,6 +30,7 @@
 // Cache layout [page][kv_head][slot][hd] (stage.py); pages resolved through the
 // device block table. Work list: int32 (seq index, q_start) pairs, host-packed.
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gllm_internal.h"
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
                     const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
                     int n_work, const int* __restrict__ block_table, int mpr, int n_heads, int n_kv, int page_size,
-                    float scale_log2, bf16* __restrict__ out) {
+                    float scale_log2, bf16* __restrict__ out, int n_split, float* __restrict__ part_o,
+                    float* __restrict__ part_ml) {
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   PrefillSmem& sm =
       *reinterpret_cast<PrefillSmem*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -385,7 +387,8 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
   pdl_trigger();
   pdl_wait();
   const int kvh = blockIdx.x;
-  const int item = n_work - 1 - (int)blockIdx.y;  // a chunk's later (longer) tiles start first
+  const int item = n_work - 1 - (int)blockIdx.y / n_split;  // a chunk's later (longer) tiles start first
+  const int split = (int)blockIdx.y % n_split;
   const int sidx = work[2 * item], q0 = work[2 * item + 1];
   const int* si = seq_info + 5 * sidx;
   const int row_id = si[0], start = si[1], n_new = si[2], tok_off = si[3];
@@ -401,6 +404,14 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
   }
   const int kv_len = start + q0 + nq[0] + nq[1];  // keys of the item's last query
   const int nb = max(nblk[0], nblk[1]);
+  // KV split (n_split > 1, few items): this CTA owns key blocks [jb, je) of the item and writes
+  // an unnormalised partial (O, running max, row sum) that attn_split_combine merges
+  const int per_split = (nb + n_split - 1) / n_split;
+  const int jb = min(nb, split * per_split), je = min(nb, jb + per_split);
+  const int nbl = je - jb;  // blocks this CTA loads
+  int tb[PTILES];           // blocks of tile t in [jb, je)
+#pragma unroll
+  for (int t = 0; t < PTILES; ++t) tb[t] = max(0, min(je, nblk[t]) - jb);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < PRING; ++s) {
@@ -443,12 +454,12 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       const int ppb = PBK / page_size;
       const uint32_t box_bytes = (uint32_t)page_size * 128;
       const uint64_t pol = policy_evict_last();  // every query tile of the sequence re-reads these pages
-      for (int f = 0; f < 2 * nb; ++f) {
+      for (int f = 0; f < 2 * nbl; ++f) {
         const int s = f % PRING;
         if (f >= PRING) mbar_wait(&sm.kv_empty[s], ((f / PRING) + 1) & 1);
         mbar_arrive_expect_tx(&sm.kv_full[s], PF_BLK_BYTES);
         const CUtensorMap* m = (f & 1) ? &v_map : &k_map;
-        const int j = f >> 1;
+        const int j = jb + (f >> 1);
         for (int pl = 0; pl < ppb; ++pl) {
           // pages past the item's last key repeat its last page (never an unmapped table entry)
           const int p = min(j * ppb + pl, n_pages - 1);
@@ -470,8 +481,8 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       if (lane == 0) mma_commit(&sm.kv_empty[f % PRING]);
       __syncwarp();
     };
-    auto issue_s = [&](int t, int j) {  // S_t = Q_t . K_j^T
-      const int s = (2 * j) % PRING;
+    auto issue_s = [&](int t, int l) {  // S_t = Q_t . K^T of local block l
+      const int s = (2 * l) % PRING;
       if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
@@ -483,27 +494,30 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int t, int j) {  // O_t += P_t . V_j, P (bf16) in S_t's first 64 columns
-      const int s = (2 * j + 1) % PRING;
+    auto issue_pv = [&](int t, int l) {  // O_t += P_t . V of local block l, P (bf16) in S_t's first 64 columns
+      const int s = (2 * l + 1) % PRING;
       if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < PBK / 16; ++kk) {
           const uint64_t db = smem_desc_sw128_mn(sm.kv[s][0] + kk * 2048, PBK * 128);
-          mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, db, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, db, idesc_o, (l > 0 || kk > 0) ? 1u : 0u);
         }
       }
       __syncwarp();
     };
-    wait_full(0);
-    for (int t = 0; t < PTILES; ++t)
-      if (nblk[t] > 0) issue_s(t, 0);
-    release(0);
-    for (int j = 0; j < nb; ++j) {
-      wait_full(2 * j + 1);
+    if (nbl > 0) {
+      wait_full(0);
+      for (int t = 0; t < PTILES; ++t)
+        if (tb[t] > 0) issue_s(t, 0);
+      release(0);
+    }
+    for (int l = 0; l < nbl; ++l) {
+      const int j = jb + l;
+      wait_full(2 * l + 1);
       if (j == nb - 1 && kv_len < nb * PBK) {
         // keys past the item's last query are never attended, but stale cache slots may hold
         // NaN/Inf bytes and P = 0 times NaN would poison O: zero those V rows
-        const int s = (2 * j + 1) % PRING;
+        const int s = (2 * l + 1) % PRING;
         const int k0 = kv_len - j * PBK;
         for (int i = lane; i < (PBK - k0) * 16; i += 32) {
           const int r = k0 + (i >> 4), half = (i >> 3) & 1, c = i & 7;
@@ -512,27 +526,27 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
         fence_proxy_async();
         __syncwarp();
       }
-      const bool next = j + 1 < nb;
-      if (next) wait_full(2 * j + 2);
+      const bool next = l + 1 < nbl;
+      if (next) wait_full(2 * l + 2);
       for (int t = 0; t < PTILES; ++t) {
-        if (j >= nblk[t]) continue;
-        mbar_wait(&sm.p_full[t], (uint32_t)(j & 1));
+        if (l >= tb[t]) continue;
+        mbar_wait(&sm.p_full[t], (uint32_t)(l & 1));
         tc_fence_after();
-        issue_pv(t, j);
-        if (j + 1 < nblk[t]) {
-          issue_s(t, j + 1);
+        issue_pv(t, l);
+        if (l + 1 < tb[t]) {
+          issue_s(t, l + 1);
         } else {
           if (lane == 0) mma_commit(&sm.o_full[t]);
           __syncwarp();
         }
       }
-      release(2 * j + 1);
-      if (next) release(2 * j + 2);
+      release(2 * l + 1);
+      if (next) release(2 * l + 2);
     }
   } else {
     // ---- softmax + epilogue of tile t: this thread owns TMEM lane / query row `row`
     const int t = warp >> 2;
-    const int tnq = t ? nq[1] : nq[0], tnb = t ? nblk[1] : nblk[0];
+    const int tnq = t ? nq[1] : nq[0], tnb = t ? tb[1] : tb[0];
     if (tnq > 0) {
       const int row = (warp & 3) * 32 + lane;
       const uint32_t t_s = tmem + t * 256 + ((uint32_t)((warp & 3) * 32) << 16);
@@ -541,8 +555,9 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       const int qfirst = start + q0 + t * QT;
       const int qpos = qfirst + (row < R ? row / G : tnq - 1);
       float m_ref = -FLT_MAX, l_sum = 0.f;
-      for (int j = 0; j < tnb; ++j) {
-        mbar_wait(&sm.s_full[t], (uint32_t)(j & 1));
+      for (int l = 0; l < tnb; ++l) {
+        const int j = jb + l;
+        mbar_wait(&sm.s_full[t], (uint32_t)(l & 1));
         tc_fence_after();
         // pass 1: row max over the block (diagonal blocks mask keys after this row's token by
         // position, so stale bytes in unattended slots never reach the max)
@@ -581,7 +596,7 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
         }
         // O (complete through block j-1: S_t(j) was issued after P.V_t(j-1)) rescaled in TMEM;
         // tcgen05.ld/st are warp-collective, so the whole warp joins when any row grows
-        if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        if (l > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll 1
           for (int c = 0; c < HD; c += 32) {
             uint32_t o[32];
@@ -607,6 +622,34 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
         tc_fence_before();
         mbar_arrive(&sm.p_full[t]);
       }
+      if (n_split > 1) {
+        // unnormalised partial: O (fp32), running max m (log2 units) and row sum of this split
+        const size_t prow = ((((size_t)item * n_split + split) * n_kv + kvh) * PTILES + t) * PM + row;
+        float* po = part_o + prow * HD;
+        if (tnb > 0) {
+          mbar_wait(&sm.o_full[t], 0);
+          tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t r32[32];
+          if (tnb > 0) {
+            tmem_ld_32x32b_x32(t_o + c, r32);  // warp-collective: all lanes
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) r32[e] = 0u;
+          }
+          if (row < R) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(po + c + e) =
+                  make_float4(__uint_as_float(r32[e]), __uint_as_float(r32[e + 1]), __uint_as_float(r32[e + 2]),
+                              __uint_as_float(r32[e + 3]));
+          }
+        }
+        if (row < R) *reinterpret_cast<float2*>(part_ml + prow * 2) = make_float2(tnb > 0 ? m_ref : -FLT_MAX, l_sum);
+      } else {
       mbar_wait(&sm.o_full[t], 0);
       tc_fence_after();
       const float inv = l_sum > 0.f ? 1.f / l_sum : 0.f;
@@ -627,6 +670,7 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
                 pack_bf16x2(__uint_as_float(r32[e + 6]) * inv, __uint_as_float(r32[e + 7]) * inv));
         }
       }
+      }
     }
   }
   tc_fence_before();
@@ -634,6 +678,41 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
   if (warp == 0) tmem_dealloc(tmem, PF_TMEM_COLS);
 }
 
+// Merge the KV-split partials of every prefill row: m = max_s m_s, O = sum_s O_s 2^(m_s - m),
+// l = sum_s l_s 2^(m_s - m), out = O / l. A warp per (item, kv head, query tile, row), 4 dims per lane.
+constexpr int CMB_ROWS = 8;  // rows (warps) per combine CTA
+template <int G>
+__global__ void __launch_bounds__(32 * CMB_ROWS)
+attn_split_combine(const int* __restrict__ seq_info, const int* __restrict__ work, int n_split, int n_heads, int n_kv,
+                   const float* __restrict__ part_o, const float* __restrict__ part_ml, bf16* __restrict__ out) {
+  constexpr int QT = PM / G;
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * CMB_ROWS + (threadIdx.x >> 5);
+  const int r = g % PM, tt = g / PM, t = tt % PTILES, kvh = (tt / PTILES) % n_kv, item = tt / PTILES / n_kv;
+  const int sidx = work[2 * item], q0 = work[2 * item + 1];
+  const int* si = seq_info + 5 * sidx;
+  const int n_new = si[2], tok_off = si[3];
+  if (r >= max(0, min(QT, n_new - (q0 + t * QT))) * G) return;
+  auto prow = [&](int s) { return ((((size_t)item * n_split + s) * n_kv + kvh) * PTILES + t) * PM + r; };
+  float m = -FLT_MAX;
+  for (int s = 0; s < n_split; ++s) m = fmaxf(m, part_ml[prow(s) * 2]);
+  float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+  float l = 0.f;
+  for (int s = 0; s < n_split; ++s) {
+    const float2 ml = *reinterpret_cast<const float2*>(part_ml + prow(s) * 2);
+    if (ml.x == -FLT_MAX) continue;
+    const float w = exp2f(ml.x - m);
+    const float4 p = *reinterpret_cast<const float4*>(part_o + prow(s) * HD + lane * 4);
+    l += ml.y * w;
+    o.x += p.x * w;
+    o.y += p.y * w;
+    o.z += p.z * w;
+    o.w += p.w * w;
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  *reinterpret_cast<uint2*>(out + (size_t)(tok_off + q0 + t * QT + r / G) * (n_heads * HD) + (kvh * G + r % G) * HD +
+                            lane * 4) = make_uint2(pack_bf16x2(o.x * inv, o.y * inv), pack_bf16x2(o.z * inv, o.w * inv));
+}
 
 // A mixed micro-batch is issued as two concurrent launches (prefill items on a forked side
 // stream, decodes on the caller's stream, joined by an event): the prefill kernel takes all of
@@ -662,10 +741,21 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_const
 // Query tokens per prefill work item (a decode, n_new == 1, is always one item).
 int attention_q_tile(int n_heads, int n_kv) { return PTILES * (PM / (n_heads / n_kv)); }
 
+// KV split of the prefill items (n_split = 1: none); partials in caller-provided device memory
+struct AttnSplit {
+  int n_split = 1;
+  float* part_o = nullptr;   // [items][n_split][n_kv][2 tiles][128 rows][128] fp32
+  float* part_ml = nullptr;  // [items][n_split][n_kv][2 tiles][128 rows][2] (max, sum)
+};
+
+size_t attention_split_bytes(int n_items, int n_split, int n_kv) {
+  return (size_t)n_items * n_split * n_kv * PTILES * PM * (HD + 2) * sizeof(float);
+}
+
 template <bool PREFILL, int G>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
                        int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
-                       float scale_log2, bf16* out, cudaStream_t st) {
+                       float scale_log2, bf16* out, cudaStream_t st, const AttnSplit& sp = AttnSplit{}) {
   constexpr size_t smem = (PREFILL ? sizeof(PrefillSmem) : sizeof(DecodeSmem)) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -684,9 +774,17 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
   if (int rc = make_tma_map_2d(&vm, v_cache, (int64_t)kv_pages * n_kv * page_size, HD, HD, page_size)) return rc;
   dim3 grid(n_kv, n_work);
   if constexpr (PREFILL) {
+    grid.y = n_work * sp.n_split;
     attn_prefill_kernel<G><<<grid, PF_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, n_work, block_table, mpr,
-                                                            n_heads, n_kv, page_size, scale_log2, out);
-    return check_launch("attention_prefill");
+                                                            n_heads, n_kv, page_size, scale_log2, out, sp.n_split,
+                                                            sp.part_o, sp.part_ml);
+    if (int rc = check_launch("attention_prefill")) return rc;
+    if (sp.n_split > 1) {
+      attn_split_combine<G><<<n_work * n_kv * PTILES * PM / CMB_ROWS, 32 * CMB_ROWS, 0, st>>>(
+          seq_info, work, sp.n_split, n_heads, n_kv, sp.part_o, sp.part_ml, out);
+      return check_launch("attention_split_combine");
+    }
+    return 0;
   } else {
     cudaError_t e = launch_kernel(attn_decode_kernel<G>, grid, dim3(ATT_THREADS), smem, st, 1, km, vm, qkv, seq_info,
                                   work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out);
@@ -719,20 +817,21 @@ static int attn_streams(AttnStreams** out) {
 template <int G>
 static int launch_attn_g(int n_prefill_work, const bf16* qkv, const int* seq_info, const int* work, int n_work,
                          const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache,
-                         int n_heads, int n_kv, int page_size, float scale_log2, bf16* out, cudaStream_t st) {
+                         int n_heads, int n_kv, int page_size, float scale_log2, bf16* out, cudaStream_t st,
+                         const AttnSplit& sp) {
   const int n_dec = n_work - n_prefill_work;
   if (n_prefill_work == 0)
     return launch_attn<false, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
                                  n_kv, page_size, scale_log2, out, st);
   if (n_dec == 0)
     return launch_attn<true, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
-                                n_kv, page_size, scale_log2, out, st);
+                                n_kv, page_size, scale_log2, out, st, sp);
   AttnStreams* ss = nullptr;
   if (int rc = attn_streams(&ss)) return rc;
   cudaEventRecord(ss->fork, st);
   cudaStreamWaitEvent(ss->side, ss->fork, 0);
   int rc = launch_attn<true, G>(qkv, seq_info, work, n_prefill_work, block_table, mpr, kv_pages, k_cache, v_cache,
-                                n_heads, n_kv, page_size, scale_log2, out, ss->side);
+                                n_heads, n_kv, page_size, scale_log2, out, ss->side, sp);
   if (rc == 0)
     rc = launch_attn<false, G>(qkv, seq_info, work + 2 * n_prefill_work, n_dec, block_table, mpr, kv_pages, k_cache,
                                v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
@@ -741,9 +840,12 @@ static int launch_attn_g(int n_prefill_work, const bf16* qkv, const int* seq_inf
   return rc;
 }
 
+// n_split: 0 = choose from the host copy of the metadata (when given) and the partial workspace;
+// >= 1 = use that many key ranges per prefill item (1 = no split).
 int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, int n_prefill_work,
                     const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache,
-                    int n_heads, int n_kv, int head_dim, int page_size, bf16* out, cudaStream_t st) {
+                    int n_heads, int n_kv, int head_dim, int page_size, bf16* out, cudaStream_t st, int n_split,
+                    const int* host_seq_info, const int* host_work, void* part_ws, size_t part_bytes) {
   if (n_work <= 0) return 0;
   if (head_dim != HD) return set_error(GLLM_ERR_INVALID, "attention supports head_dim 128 only (got %d)", head_dim);
   if (n_heads % n_kv) return set_error(GLLM_ERR_INVALID, "bad GQA grouping");
@@ -751,12 +853,52 @@ int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n
   if (n_prefill_work < 0 || n_prefill_work > n_work) return set_error(GLLM_ERR_INVALID, "bad n_prefill_work");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
   const int pf = n_prefill_work;
+  AttnSplit sp;
+  // Automatic KV split is opt-in (GLLM_ATTN_SPLIT=1): +8% on an isolated 640-token chunk after 6k
+  // cached keys, but -7% on the prefill attention of the C5 serving bench, where the prefill
+  // launch shares the SMs with the concurrent decode launch.
+  static const bool auto_split = [] {
+    const char* e = getenv("GLLM_ATTN_SPLIT");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  if (pf > 0 && n_split == 0 && auto_split && host_seq_info && host_work && part_ws) {
+    // Few prefill CTAs (one per SM): cutting each item's key range into S parts trades wave
+    // quantization for per-CTA fixed cost (Q load, pipeline fill, partial write + combine),
+    // measured at ~8 key blocks. Pick S minimising waves(S) x (blocks per item / S + 8).
+    const int sms = device_sm_count(), ctas = pf * n_kv;
+    const int item_tokens = attention_q_tile(n_heads, n_kv);
+    if (ctas < 2 * sms) {
+      long blocks = 0;
+      for (int i = 0; i < pf; ++i) {
+        const int* si = host_seq_info + 5 * host_work[2 * i];
+        const int last = min(si[2], host_work[2 * i + 1] + item_tokens);
+        blocks += (si[1] + last + PBK - 1) / PBK;
+      }
+      const double per_item = (double)blocks / pf;
+      double best = 0.0;
+      for (int S = 1; S <= 8; ++S) {
+        const double t = (double)((ctas * S + sms - 1) / sms) * (per_item / S + 8.0);
+        if (S == 1 || t < best) {
+          best = t;
+          n_split = S;
+        }
+      }
+    }
+  }
+  if (n_split > 1 && pf > 0) {
+    while (n_split > 1 && attention_split_bytes(pf, n_split, n_kv) > part_bytes) --n_split;
+    if (n_split > 1) {
+      sp.n_split = n_split;
+      sp.part_o = reinterpret_cast<float*>(part_ws);
+      sp.part_ml = sp.part_o + (size_t)pf * n_split * n_kv * PTILES * PM * HD;
+    }
+  }
   switch (n_heads / n_kv) {
-    case 1: return launch_attn_g<1>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 2: return launch_attn_g<2>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 4: return launch_attn_g<4>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 5: return launch_attn_g<5>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
-    case 8: return launch_attn_g<8>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+    case 1: return launch_attn_g<1>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
+    case 2: return launch_attn_g<2>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
+    case 4: return launch_attn_g<4>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
+    case 5: return launch_attn_g<5>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
+    case 8: return launch_attn_g<8>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
     default: return set_error(GLLM_ERR_INVALID, "unsupported GQA group %d", n_heads / n_kv);
   }
 }

@@ -579,7 +579,10 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     const char* e = getenv("GLLM_GEMM_CG");
     return e ? atoi(e) : 2;
   }();
-  const int cg = (cg_pref == 2 && splits == 1 && m_tiles >= 2 && bn >= 128) ? 2 : 1;
+  // (an odd count of 128-row tiles leaves half of the last 256-row pair tile empty: only worth it
+  // once that is a small share of the work)
+  const int cg = (cg_pref == 2 && splits == 1 && m_tiles >= 2 && bn >= 128 && (m_tiles % 2 == 0 || m_tiles >= 8))
+                     ? 2 : 1;
   CUtensorMap ma, mb;
   const int a_rows = a_rows_alloc > M ? a_rows_alloc : M;
   if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;

@@ -108,8 +108,11 @@ int commit_tokens(const int* seq_info, int n_seqs, const int* sampled, int* toke
 
 // attention.cu
 int attention_q_tile(int n_heads, int n_kv);
+// n_split: 0 = auto (needs host_seq_info / host_work and part_ws), 1 = no KV split, >1 = forced
 int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n_work, int n_prefill_work,
                     const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int head_dim,
-                    int page_size, bf16* out, cudaStream_t st);
+                    int page_size, bf16* out, cudaStream_t st, int n_split = 1, const int* host_seq_info = nullptr,
+                    const int* host_work = nullptr, void* part_ws = nullptr, size_t part_bytes = 0);
+size_t attention_split_bytes(int n_items, int n_split, int n_kv);
 
 }  // namespace gllm

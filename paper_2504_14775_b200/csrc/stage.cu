@@ -142,6 +142,8 @@ struct StageWs {
   int *tok_pos, *tok_slot, *tok_id, *emit_rows;
   float* gemm;
   size_t gemm_bytes;
+  void* attn_part;  // prefill KV-split partials
+  size_t attn_part_bytes;
   size_t total;
 };
 
@@ -172,6 +174,10 @@ static StageWs carve(const gllm_dims& d, uint8_t* base) {
   // split-K partials: splits * tiles <= 2 * SMs, tile <= 128 x 256 fp32
   w.gemm_bytes = 16384 + (size_t)2 * 160 * 128 * 256 * 4;
   w.gemm = (float*)take(w.gemm_bytes);
+  // KV-split partials: splitting only happens below two waves of prefill CTAs (< 2 x 148 items x kv
+  // heads) and keeps items x kv heads x splits <= 2 x 148 + items x kv heads
+  w.attn_part_bytes = attention_split_bytes(4 * 160, 1, 1);
+  w.attn_part = take(w.attn_part_bytes);
   w.total = off;
   return w;
 }
@@ -267,7 +273,10 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
       return rc;
     if ((rc = prof_call(P_ATTN, att_flops, att_bytes, st, [&] {
            return attention_paged(w.qkv, mv.seq_info, mv.work, B.n_work, B.n_prefill_work, S.block_table,
-                                  d.max_pages_per_row, d.num_pages, kc, vc, H, KV, HDIM, d.page_size, w.attn, st);
+                                  d.max_pages_per_row, d.num_pages, kc, vc, H, KV, HDIM, d.page_size, w.attn, st,
+                                  /*n_split=*/0, B.host_seq_info,
+                                  B.host_seq_info ? B.host_seq_info + GLLM_SEQ_FIELDS * B.n_seqs : nullptr,
+                                  w.attn_part, w.attn_part_bytes);
          })))
       return rc;
     GLLM_CHECK(w.attn, (size_t)T * H * HDIM, "attention", l);
@@ -405,6 +414,24 @@ int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_
                          kv_pages,
                          (const bf16*)k_cache, (const bf16*)v_cache, n_heads, n_kv_heads, head_dim, page_size,
                          (bf16*)out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int gllm_attn_mixed_paged_split(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
+                                int n_prefill_work, const int32_t* block_table, int max_pages_per_row, int kv_pages,
+                                const void* k_cache, const void* v_cache, int n_heads, int n_kv_heads, int head_dim,
+                                int page_size, void* out, int n_split, void* workspace, size_t workspace_bytes,
+                                gllm_stream_t stream) {
+  if (n_split < 1) return set_error(GLLM_ERR_INVALID, "n_split must be >= 1");
+  if (n_split > 1 && workspace_bytes < attention_split_bytes(n_prefill_work, n_split, n_kv_heads))
+    return set_error(GLLM_ERR_INVALID, "attention split workspace too small");
+  return attention_paged((const bf16*)qkv, seq_info, work, n_work, n_prefill_work, block_table, max_pages_per_row,
+                         kv_pages, (const bf16*)k_cache, (const bf16*)v_cache, n_heads, n_kv_heads, head_dim,
+                         page_size, (bf16*)out, reinterpret_cast<cudaStream_t>(stream), n_split, nullptr, nullptr,
+                         workspace, workspace_bytes);
+}
+
+size_t gllm_attn_split_workspace_bytes(int n_prefill_work, int n_split, int n_kv_heads) {
+  return attention_split_bytes(n_prefill_work, n_split, n_kv_heads);
 }
 
 int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream) {

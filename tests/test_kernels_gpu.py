@@ -224,10 +224,13 @@ def _paged_setup(n_kv, hd, ps, ctx_lens, num_pages, seed=0):
 LONG_SEQS = [(37, 1), (1500, 517), (0, 300), (2000, 129), (4, 1), (900, 2)]
 
 
-@pytest.mark.parametrize("n_heads,n_kv,ps,seqs", [(32, 8, 16, None), (40, 8, 16, None), (64, 8, 16, None),
-                                                  (2, 1, 16, None), (32, 8, 16, LONG_SEQS), (40, 8, 8, LONG_SEQS),
-                                                  (64, 8, 16, LONG_SEQS)])
-def test_attention_mixed(lib, n_heads, n_kv, ps, seqs):
+@pytest.mark.parametrize("n_heads,n_kv,ps,seqs,n_split", [(32, 8, 16, None, 1), (40, 8, 16, None, 1),
+                                                          (64, 8, 16, None, 1), (2, 1, 16, None, 1),
+                                                          (32, 8, 16, LONG_SEQS, 1), (40, 8, 8, LONG_SEQS, 1),
+                                                          (64, 8, 16, LONG_SEQS, 1), (32, 8, 16, LONG_SEQS, 3),
+                                                          (40, 8, 8, LONG_SEQS, 2), (64, 8, 16, LONG_SEQS, 8),
+                                                          (32, 8, 16, None, 4)])
+def test_attention_mixed(lib, n_heads, n_kv, ps, seqs, n_split):
     hd = 128
     # (start, n_new): decodes, a first chunk, a later chunk, a long decode
     seqs = seqs or [(37, 1), (0, 45), (100, 70), (511, 1), (15, 1), (3, 200)]
@@ -247,8 +250,16 @@ def test_attention_mixed(lib, n_heads, n_kv, ps, seqs):
     info_t = torch.tensor(info, dtype=torch.int32, device="cuda")
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
     out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
-    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), n_pf, table.data_ptr(),
-             mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
+    if n_split == 1:
+        lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), n_pf,
+                 table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(),
+                 lib.stream_handle())
+    else:
+        ws = torch.empty(lib.load().gllm_attn_split_workspace_bytes(n_pf, n_split, n_kv), dtype=torch.uint8,
+                         device="cuda")
+        lib.call("gllm_attn_mixed_paged_split", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), n_pf,
+                 table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(),
+                 n_split, ws.data_ptr(), ws.numel(), lib.stream_handle())
     torch.cuda.synchronize()
     g = n_heads // n_kv
     for i, (s, n) in enumerate(seqs):

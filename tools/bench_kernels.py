@@ -34,7 +34,7 @@ def timeit(fn, reps=10):
     return ts[len(ts) // 2]
 
 
-def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False):
+def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False, split=1):
     hd = 128
     ctx = [s + n for s, n in seqs]
     pages_per = [-(-c // ps) for c in ctx]
@@ -62,8 +62,16 @@ def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False):
     info = torch.tensor(info, dtype=torch.int32, device="cuda")
     work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
     st = native.stream_handle()
-    fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work), max(int(force_mixed), sum(1 for i, _ in work if seqs[i][1] > 1)),
-                             table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), st)
+    n_pf = max(int(force_mixed), sum(1 for i, _ in work if seqs[i][1] > 1))
+    if split > 1:
+        ws = torch.empty(native.load().gllm_attn_split_workspace_bytes(n_pf, split, n_kv), dtype=torch.uint8, device="cuda")
+        fn = lambda: native.call("gllm_attn_mixed_paged_split", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work),
+                                 n_pf, table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd,
+                                 ps, out.data_ptr(), split, ws.data_ptr(), ws.numel(), st)
+    else:
+        fn = lambda: native.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work),
+                                 n_pf, table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd,
+                                 ps, out.data_ptr(), st)
     ms = timeit(fn)
     kv_bytes = sum(ctx) * n_kv * hd * 2 * 2 + T * n_heads * hd * 2 * 2
     flops = sum(4 * n_heads * hd * (n * s + n * (n + 1) / 2) for s, n in seqs)
@@ -119,6 +127,10 @@ if __name__ == "__main__":
         attn_case("prefill_2048_from0_8b", [(0, 2048)])
         attn_case("prefill_2048_after4096_70b", [(4096, 2048)], n_heads=64)
         attn_case("prefill_640_after6000_70b", [(6000, 640)], n_heads=64)
+        attn_case("prefill_640_after6000_70b_split2", [(6000, 640)], n_heads=64, split=2)
+        attn_case("prefill_640_after6000_70b_split4", [(6000, 640)], n_heads=64, split=4)
+        attn_case("prefill_2x256_after7000_70b_split8", [(7000, 256)] * 2, n_heads=64, split=8)
+        attn_case("prefill_2x256_after7000_70b", [(7000, 256)] * 2, n_heads=64)
         attn_case("prefill_4x512_after2000_qwen", [(2000, 512)] * 4, n_heads=40)
         attn_case("decode256_qwen", [(600, 1)] * 256, n_heads=40)
         attn_case("decode128_70b", [(4000, 1)] * 128, n_heads=64)

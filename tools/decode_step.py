@@ -1,0 +1,73 @@
+"""Decode-only step time at a fixed batch size (the low-load TPOT regime), on one B200.
+
+    python tools/decode_step.py --model qwen2.5-14b --batch 4 [--ctx 512] [--steps 30]
+
+N requests (prompt --ctx tokens, long outputs) all arrive at t=0; the virtual-clock engine
+(reference scheduling) drives LocalExecutor until every request decodes, then the device time
+of each decode-only micro-batch (N tokens, no prefill) is read from CUDA events. Prints the
+median ms per step and its ratio to the weight-streaming floor (stage weights / measured HBM
+bandwidth). Run under `ncu --nvtx --nvtx-include decode_timed/` for a per-kernel split.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="qwen2.5-14b")
+    ap.add_argument("--batch", type=int, default=4)
+    ap.add_argument("--ctx", type=int, default=512)
+    ap.add_argument("--steps", type=int, default=30)
+    a = ap.parse_args()
+
+    import torch
+
+    from paper_2504_14775_b200 import Engine, KvConfig, PipelineConfig, RequestSpec, ThrottleConfig
+    from paper_2504_14775_b200.executor import LocalExecutor
+    from paper_2504_14775_b200.modelspec import MODELS
+
+    spec = MODELS[a.model]
+    warm = 40
+    reqs = [RequestSpec(i, 0.0, a.ctx, warm + a.steps + 8) for i in range(a.batch)]
+    pages = a.batch * (-(-(a.ctx + warm + a.steps + 16) // 16)) + 64
+    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, max_tokens=2048, max_emit=max(a.batch, 32), seed=0)
+    eng = Engine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(pages, 16), throttle=ThrottleConfig(),
+                 executor=ex)
+    decode_only, ranged = [], False
+    while eng.step():
+        its = eng._iters
+        if its and its[-1].prefill_tokens == 0 and its[-1].decode_tokens == a.batch:
+            decode_only.append(its[-1].batch_seq)
+            if len(decode_only) == warm // 2 and not ranged:
+                torch.cuda.synchronize()
+                torch.cuda.nvtx.range_push("decode_timed")
+                ranged = True
+            if len(decode_only) >= warm // 2 + a.steps:
+                break
+    torch.cuda.synchronize()
+    if ranged:
+        torch.cuda.nvtx.range_pop()
+    dev = ex.batch_device_ms()
+    ms = [dev[s] for s in decode_only[warm // 2:] if s in dev]
+    w_bytes = spec.n_layers * spec.params_per_layer * 2 + spec.vocab * spec.d_model * 2
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except (OSError, KeyError, ValueError):
+        hbm = 6650.0
+    floor_ms = w_bytes / (hbm * 1e9) * 1e3
+    med = statistics.median(ms)
+    print(json.dumps({"model": a.model, "batch": a.batch, "ctx": a.ctx, "steps": len(ms), "ms_per_step": round(med, 3),
+                      "weight_floor_ms": round(floor_ms, 3), "frac_of_floor": round(floor_ms / med, 3)}))
+
+
+if __name__ == "__main__":
+    main()
