@@ -544,11 +544,15 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   const int num_sms = device_sm_count();
   const int m_tiles = (M + BM - 1) / BM;
   const int min_bn = (swiglu || qkv) ? 128 : 64;
-  // Tile width: widest that still yields at least one wave of CTAs.
+  // Tile width. Up to 4 row tiles (M <= 512) the GEMM streams its weights and every CTA must
+  // also ingest its A rows once per N tile: keep BN = 256 (A re-read by the fewest N tiles) and
+  // fill the machine with split-K below. Beyond that: widest BN that still yields one wave.
   int bn = force_bn;
   if (bn == 0) {
     bn = 256;
-    while (bn > min_bn && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
+    if (m_tiles > 4)
+      while (bn > min_bn && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
+    while (bn > min_bn && N % bn) bn >>= 1;
     if (N % bn) bn = (N % 128 == 0) ? 128 : 64;
   }
   if ((swiglu || qkv) && bn < 128) return set_error(GLLM_ERR_INVALID, "swiglu/qkv gemm needs BN >= 128");
@@ -558,9 +562,23 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   if (splits == 0) {
     splits = 1;
     const long tiles = (long)n_tiles * m_tiles;
-    // Split K only when one wave is not filled (HBM-bound weight streaming for small M).
-    while (tiles * splits * 2 <= num_sms * 2 && total_kb / (splits * 2) >= 4) splits *= 2;
-    if (tiles * splits < num_sms / 2 && total_kb / (splits * 2) >= 2) splits *= 2;
+    // Split K only when one wave is not filled (HBM-bound weight streaming for small M). The
+    // split count minimises waves(s) / s -- the time of a wave shrinks with 1/s -- plus the fp32
+    // partials (written and re-read: 8 B per output per split, against the 2 B per weight the
+    // GEMM streams anyway): 40 tiles -> 3 splits (1 wave of 1/3 tiles) rather than 4 (160
+    // units = 2 waves of 1/4 tiles).
+    if (tiles < num_sms) {
+      double best = 1e30;
+      const double partial_cost = 2.0 * M / K;  // partial bytes per split / weight bytes
+      for (int s = 1; s <= 16 && total_kb / s >= 4; ++s) {
+        if (s > 1 && (workspace == nullptr || ws_bytes < GEMM_WS_HEAD_BYTES + (size_t)s * M * N * sizeof(float))) break;
+        const double c = (double)((tiles * s + num_sms - 1) / num_sms) / s + (s > 1 ? s * partial_cost : 0.0);
+        if (c < best) {
+          best = c;
+          splits = s;
+        }
+      }
+    }
   }
   splits = splits < 1 ? 1 : (splits > total_kb ? total_kb : splits);
   const int kbps = (total_kb + splits - 1) / splits;

@@ -172,7 +172,7 @@ static StageWs carve(const gllm_dims& d, uint8_t* base) {
   w.tok_id = (int*)take(T * 4);
   w.emit_rows = (int*)take(E * 4);
   // split-K partials: splits * tiles <= 2 * SMs, tile <= 128 x 256 fp32
-  w.gemm_bytes = 16384 + (size_t)2 * 160 * 128 * 256 * 4;
+  w.gemm_bytes = 16384 + (size_t)3 * 160 * 128 * 256 * 4;
   w.gemm = (float*)take(w.gemm_bytes);
   // KV-split partials: splitting only happens below two waves of prefill CTAs (< 2 x 148 items x kv
   // heads) and keeps items x kv heads x splits <= 2 x 148 + items x kv heads
