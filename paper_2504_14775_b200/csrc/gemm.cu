@@ -547,11 +547,32 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   // Tile width. Up to 4 row tiles (M <= 512) the GEMM streams its weights and every CTA must
   // also ingest its A rows once per N tile: keep BN = 256 (A re-read by the fewest N tiles) and
   // fill the machine with split-K below. Beyond that: widest BN that still yields one wave.
-  int bn = force_bn;
+  // Beyond 4 row tiles the GEMM is compute-bound: pick (cta_group, BN) by modelled time = waves x
+  // per-SM tile work / relative MMA efficiency, the efficiency set by the smem operand traffic
+  // per MMA cycle (1-CTA BN=256: 96 B/clk; 2-CTA BN=256: 64 B/clk; 1-CTA BN=128: 128 B/clk).
+  static const int cg_pref = [] {
+    const char* e = getenv("GLLM_GEMM_CG");  // GLLM_GEMM_CG=1 forces 1-CTA tiles (A/B runs)
+    return e ? atoi(e) : 2;
+  }();
+  int bn = force_bn, cg_pick = 0;
   if (bn == 0) {
     bn = 256;
-    if (m_tiles > 4)
-      while (bn > min_bn && ((N % bn) != 0 || (long)(N / bn) * m_tiles < num_sms)) bn >>= 1;
+    if (m_tiles > 4 && force_splits == 0) {
+      struct Cand { int cg, bn; double eff; };
+      const Cand cands[] = {{2, 256, 0.85}, {2, 128, 0.75}, {1, 256, 0.75}, {1, 128, 0.55}, {1, 64, 0.37}};
+      double best = 1e30;
+      for (const Cand& c : cands) {
+        if (N % c.bn || c.bn < min_bn || (c.cg == 2 && cg_pref != 2)) continue;
+        const long units = (long)((M + BM * c.cg - 1) / (BM * c.cg)) * (N / c.bn);
+        const long slots = num_sms / c.cg;
+        const double t = (double)((units + slots - 1) / slots) * c.bn / c.eff;
+        if (t < best) {
+          best = t;
+          bn = c.bn;
+          cg_pick = c.cg;
+        }
+      }
+    }
     while (bn > min_bn && N % bn) bn >>= 1;
     if (N % bn) bn = (N % 128 == 0) ? 128 : 64;
   }
@@ -591,16 +612,11 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       return set_error(GLLM_ERR_INVALID, "gemm split-K workspace too small (%zu < %zu)", ws_bytes, need);
     partial = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + GEMM_WS_HEAD_BYTES);
   }
-  // 2-CTA (cta_group::2) tiles once there is more than one 128-row tile and no split-K; decode
-  // micro-batches (M <= 128) stay on the 1-CTA kernel. GLLM_GEMM_CG=1 forces 1-CTA (A/B runs).
-  static const int cg_pref = [] {
-    const char* e = getenv("GLLM_GEMM_CG");
-    return e ? atoi(e) : 2;
-  }();
-  // (an odd count of 128-row tiles leaves half of the last 256-row pair tile empty: only worth it
-  // once that is a small share of the work)
-  const int cg = (cg_pref == 2 && splits == 1 && m_tiles >= 2 && bn >= 128 && (m_tiles % 2 == 0 || m_tiles >= 8))
-                     ? 2 : 1;
+  // 2-CTA (cta_group::2) tiles: the modelled pick above, else (forced tiles, <= 4 row tiles
+  // without split-K) whenever the 128-row tiles pair up evenly.
+  const int cg = splits > 1 ? 1
+                 : cg_pick    ? cg_pick
+                              : ((cg_pref == 2 && m_tiles >= 2 && bn >= 128 && m_tiles % 2 == 0) ? 2 : 1);
   CUtensorMap ma, mb;
   const int a_rows = a_rows_alloc > M ? a_rows_alloc : M;
   if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;
