@@ -68,6 +68,10 @@ typedef struct gllm_dims {
   int max_seq_len;  /* token-history row length */
   int max_tokens;   /* packed tokens per micro-batch (workspace sizing) */
   int max_emit;     /* sampled rows per micro-batch (workspace sizing) */
+  int fused_norm;   /* 1: attn_norm / mlp_norm are folded into the columns of w_qkv / w_gate_up (the
+                       norm vectors are ignored): no RMSNorm launches, the row scale is applied in the
+                       QKV / gate-up GEMM epilogues and its statistics are accumulated by the O / down
+                       GEMM epilogues. 0: separate RMSNorm kernels. */
 } gllm_dims;
 
 typedef struct gllm_layer {

@@ -44,7 +44,10 @@ template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, int n0, int split, int M, int N,
                                               bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
                                               const bf16* __restrict__ residual, int ldr,
-                                              float* __restrict__ partial, const QkvRopeArgs& qa) {
+                                              float* __restrict__ partial, const QkvRopeArgs& qa,
+                                              const RowNorm& nm) {
+  // fused RMSNorm: this row's scale for the GEMM output (ss_in), and its output statistics (ss_out)
+  const float rs = (nm.ss_in != nullptr && row < M) ? rsqrtf(nm.ss_in[row] / nm.d + nm.eps) : 1.f;
   if constexpr (MODE == EPI_QKV_ROPE) {
     // Head-aligned tile: columns [128h, 128h+128) are one whole head of this token row, so the
     // rotate-half pairs (d, d+64) are thread-local. q heads are rotated and written back to C;
@@ -68,8 +71,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
         float a[32], b[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          a[j] = __uint_as_float(x1[j]);
-          b[j] = __uint_as_float(x2[j]);
+          a[j] = __uint_as_float(x1[j]) * rs;
+          b[j] = __uint_as_float(x2[j]) * rs;
         }
         if (bias != nullptr) {
 #pragma unroll
@@ -130,8 +133,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
         uint32_t packed[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          float a0 = bf2f(f2bf(__uint_as_float(g[2 * j]))), a1 = bf2f(f2bf(__uint_as_float(g[2 * j + 1])));
-          const float b0 = bf2f(f2bf(__uint_as_float(u[2 * j]))), b1 = bf2f(f2bf(__uint_as_float(u[2 * j + 1])));
+          float a0 = bf2f(f2bf(__uint_as_float(g[2 * j]) * rs)), a1 = bf2f(f2bf(__uint_as_float(g[2 * j + 1]) * rs));
+          const float b0 = bf2f(f2bf(__uint_as_float(u[2 * j]) * rs)), b1 = bf2f(f2bf(__uint_as_float(u[2 * j + 1]) * rs));
           a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
           a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
           packed[j] = pack_bf16x2(a0 * b0, a1 * b1);
@@ -143,6 +146,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
       }
     }
   } else {
+    float ss = 0.f;  // sum of squares of this row's bf16 outputs (fused-norm statistics)
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
@@ -159,7 +163,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
       } else {
         float v[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * rs;
         if (bias != nullptr) {
           const uint4* bp = reinterpret_cast<const uint4*>(bias + col);
 #pragma unroll
@@ -188,8 +192,16 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
         for (int j = 0; j < 4; ++j)
           dst[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
                               pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+        if (nm.ss_out != nullptr) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float q = bf2f(f2bf(v[j]));
+            ss = fmaf(q, q, ss);
+          }
+        }
       }
     }
+    if (nm.ss_out != nullptr && row < M) atomicAdd(nm.ss_out + row, ss);
   }
 }
 
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                   int M, int N, int K, int k_blocks_per_split, int n_splits, bf16* __restrict__ C, int ldc,
                   const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
-                  float* __restrict__ partial, const QkvRopeArgs qa) {
+                  float* __restrict__ partial, const QkvRopeArgs qa, const RowNorm nm) {
   static_assert(CG == 1 || CG == 2, "cta_group 1 or 2");
   using L = GemmSmem<BN / CG, STAGES>;   // per-CTA stage: 128 A rows + BN/CG B rows
   extern __shared__ uint8_t smem_raw[];
@@ -333,6 +345,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
   } else {
     // Epilogue warps 2-5: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
     pdl_wait();  // C / residual / KV cache are shared with the predecessor
+    if (nm.zero != nullptr && blockIdx.x == 0)
+      for (int i = threadIdx.x - 64; i < nm.zero_n; i += 128) nm.zero[i] = 0.f;
     const int q = warp & 3;
     const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(acc_empty), 0) : 0u;
     int lt = 0;
@@ -344,7 +358,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
       tc_fence_after();
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       epilogue_tile<BN, MODE>(lane_base, m0 + (int)rank * BM + q * 32 + lane, n0, split, M, N, C, ldc, bias,
-                              residual, ldr, partial, qa);
+                              residual, ldr, partial, qa, nm);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -361,7 +375,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
 
 // Sum split-K partials [splits, M, N] fp32 and apply the epilogue; 8 columns per thread.
 __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int M, int N, bf16* __restrict__ C,
-                              int ldc, const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr) {
+                              int ldc, const bf16* __restrict__ bias, const bf16* __restrict__ residual, int ldr,
+                              const RowNorm nm) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t groups = (size_t)M * (N / 8);
   if (idx >= groups) return;
@@ -377,6 +392,11 @@ __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int
     const float4* p = reinterpret_cast<const float4*>(partial + ((size_t)s * M + row) * N + col);
     float4 a = p[0], b = p[1];
     v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w; v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
+  }
+  if (nm.ss_in != nullptr) {
+    const float rs = rsqrtf(nm.ss_in[row] / nm.d + nm.eps);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] *= rs;
   }
   if (bias != nullptr) {
     uint4 u = *reinterpret_cast<const uint4*>(bias + col);
@@ -400,12 +420,21 @@ __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int
   }
   *reinterpret_cast<uint4*>(C + (size_t)row * ldc + col) =
       make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+  if (nm.ss_out != nullptr) {
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float q = bf2f(f2bf(v[j]));
+      ss = fmaf(q, q, ss);
+    }
+    atomicAdd(nm.ss_out + row, ss);
+  }
 }
 
 // Split-K reduce for the SwiGLU GEMM: N = 2*d_ff interleaved columns -> act[M, d_ff].
 // Output column o reads gate column 128*(o/64) + o%64 and up column gate + 64.
 __global__ void splitk_reduce_swiglu(const float* __restrict__ partial, int splits, int M, int N,
-                                     bf16* __restrict__ C, int ldc) {
+                                     bf16* __restrict__ C, int ldc, const RowNorm nm) {
   const int half = N / 2;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)M * (half / 8)) return;
@@ -423,13 +452,14 @@ __global__ void splitk_reduce_swiglu(const float* __restrict__ partial, int spli
       u[j] += base[gcol + 64 + j];
     }
   }
+  const float rs = nm.ss_in != nullptr ? rsqrtf(nm.ss_in[row] / nm.d + nm.eps) : 1.f;
   uint32_t pk[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    float a0 = bf2f(f2bf(g[2 * j])), a1 = bf2f(f2bf(g[2 * j + 1]));
+    float a0 = bf2f(f2bf(g[2 * j] * rs)), a1 = bf2f(f2bf(g[2 * j + 1] * rs));
     a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
     a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
-    pk[j] = pack_bf16x2(a0 * bf2f(f2bf(u[2 * j])), a1 * bf2f(f2bf(u[2 * j + 1])));
+    pk[j] = pack_bf16x2(a0 * bf2f(f2bf(u[2 * j] * rs)), a1 * bf2f(f2bf(u[2 * j + 1] * rs)));
   }
   *reinterpret_cast<uint4*>(C + (size_t)row * ldc + o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
 }
@@ -508,7 +538,7 @@ int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t col
 template <int BN, int STAGES, int MODE, int CG = 1>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K, int splits, int kbps,
                        bf16* C, int ldc, const bf16* bias, const bf16* res, int ldr, float* partial,
-                       cudaStream_t st, const QkvRopeArgs& qa = QkvRopeArgs{}) {
+                       cudaStream_t st, const RowNorm& nm, const QkvRopeArgs& qa = QkvRopeArgs{}) {
   constexpr int smem = GemmSmem<BN / CG, STAGES>::TOTAL;
   auto kern = gemm_bf16_tcgen05<BN, STAGES, MODE, CG>;
   static bool attr_done = false;
@@ -521,7 +551,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   const long slots = device_sm_count() / CG;
   const int clusters = (int)(units < slots ? units : slots);
   cudaError_t e = launch_kernel(kern, dim3(CG * clusters), dim3(GEMM_THREADS), smem, st, CG, ma, mb, M, N, K, kbps,
-                                splits, C, ldc, bias, res, ldr, partial, qa);
+                                splits, C, ldc, bias, res, ldr, partial, qa, nm);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
   return check_launch("gemm_bf16_tcgen05");
 }
@@ -531,14 +561,14 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
 static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
                      const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn,
                      int force_splits, int swiglu, void* workspace, size_t ws_bytes, cudaStream_t st,
-                     const QkvRopeArgs* qkv = nullptr) {
+                     const QkvRopeArgs* qkv, const RowNorm& nm) {
   if (M <= 0) return 0;
   if (K % BK != 0 || N % 64 != 0) return set_error(GLLM_ERR_INVALID, "gemm needs K %% 64 == 0 and N %% 64 == 0 (K=%d N=%d)", K, N);
   // decode-sized M: swap-AB stream-K weight streaming (gemm_skinny.cu)
   if (force_splits == 0 && force_bn == 0 && gemm_skinny_eligible(M, N, K) &&
       ws_bytes >= gemm_skinny_workspace_bytes(M, N, K) && !(swiglu && (bias || residual)))
     return gemm_skinny(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, swiglu ? EPI_SWIGLU : (qkv ? EPI_QKV_ROPE : EPI_STORE),
-                       bias, residual, ldr, qkv, workspace, ws_bytes, st);
+                       bias, residual, ldr, qkv, workspace, ws_bytes, st, nm);
   if (ldc % 8 || (residual && ldr % 8)) return set_error(GLLM_ERR_INVALID, "gemm output pitch must be a multiple of 8");
   if (swiglu && (N % 128 || bias || residual)) return set_error(GLLM_ERR_INVALID, "swiglu gemm needs N %% 128 == 0, no bias/residual");
   const int num_sms = device_sm_count();
@@ -625,7 +655,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   if (qkv && splits > 1) {
     // small-M QKV: split-K plain GEMM, then the standalone RoPE + KV-write kernel
     int rc = gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, bias, nullptr, 0, a_rows_alloc, force_bn, splits, 0,
-                       workspace, ws_bytes, st, nullptr);
+                       workspace, ws_bytes, st, nullptr, nm);
     if (rc) return rc;
     return rope_kv_write(C, M, qkv->n_heads, qkv->n_kv, 128, qkv->tok_pos, qkv->tok_slot, qkv->rope, qkv->k_cache,
                          qkv->v_cache, qkv->page_size, st);
@@ -635,28 +665,28 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   if (bn == BNV) {                                                                                           \
     if (mode == EPI_STORE)                                                                                   \
       rc = launch_gemm<BNV, ST, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual, ldr,       \
-                                           nullptr, st);                                                     \
+                                           nullptr, st, nm);                                                     \
     else if (mode == EPI_PARTIAL_F32)                                                                        \
       rc = launch_gemm<BNV, ST, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0, \
-                                                 partial, st);                                               \
+                                                 partial, st, nm);                                               \
     else if (mode == EPI_SWIGLU)                                                                             \
       rc = launch_gemm<BNV, ST, EPI_SWIGLU>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0,      \
-                                            nullptr, st);                                                    \
+                                            nullptr, st, nm);                                                    \
     else                                                                                                     \
       rc = launch_gemm<BNV, ST, EPI_QKV_ROPE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, nullptr, 0,       \
-                                              nullptr, st, *qkv);                                            \
+                                              nullptr, st, nm, *qkv);                                            \
   }
 #define GLLM_GEMM_CASE2(BNV, ST)                                                                              \
   if (bn == BNV) {                                                                                            \
     if (mode == EPI_STORE)                                                                                    \
       rc = launch_gemm<BNV, ST, EPI_STORE, 2>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual, ldr,     \
-                                              nullptr, st);                                                   \
+                                              nullptr, st, nm);                                                   \
     else if (mode == EPI_SWIGLU)                                                                              \
       rc = launch_gemm<BNV, ST, EPI_SWIGLU, 2>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr, nullptr, 0,    \
-                                               nullptr, st);                                                  \
+                                               nullptr, st, nm);                                                  \
     else                                                                                                      \
       rc = launch_gemm<BNV, ST, EPI_QKV_ROPE, 2>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, nullptr, 0,     \
-                                                 nullptr, st, *qkv);                                          \
+                                                 nullptr, st, nm, *qkv);                                          \
   }
   if (cg == 2) {
     GLLM_GEMM_CASE2(256, 6)
@@ -665,9 +695,9 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   GLLM_GEMM_CASE(256, 4)
   else GLLM_GEMM_CASE(128, 6) else if (bn == 64 && !swiglu && !qkv) {
     rc = mode == EPI_STORE ? launch_gemm<64, 8, EPI_STORE>(ma, mb, M, N, K, splits, kbps, C, ldc, bias, residual,
-                                                           ldr, nullptr, st)
+                                                           ldr, nullptr, st, nm)
                            : launch_gemm<64, 8, EPI_PARTIAL_F32>(ma, mb, M, N, K, splits, kbps, C, ldc, nullptr,
-                                                                 nullptr, 0, partial, st);
+                                                                 nullptr, 0, partial, st, nm);
   } else return set_error(GLLM_ERR_INVALID, "bad BN %d (swiglu/qkv need >= 128)", bn);
 #undef GLLM_GEMM_CASE
 #undef GLLM_GEMM_CASE2
@@ -677,12 +707,12 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     if (swiglu) {
       const size_t groups = (size_t)M * (N / 2 / 8);
       splitk_reduce_swiglu<<<(unsigned)((groups + threads - 1) / threads), threads, 0, st>>>(partial, splits, M, N,
-                                                                                             C, ldc);
+                                                                                             C, ldc, nm);
       rc = check_launch("splitk_reduce_swiglu");
     } else {
       const size_t groups = (size_t)M * (N / 8);
       splitk_reduce<<<(unsigned)((groups + threads - 1) / threads), threads, 0, st>>>(partial, splits, M, N, C, ldc,
-                                                                                     bias, residual, ldr);
+                                                                                     bias, residual, ldr, nm);
       rc = check_launch("splitk_reduce");
     }
   }
@@ -691,26 +721,27 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
 
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
               const bf16* bias, const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits,
-              void* workspace, size_t ws_bytes, cudaStream_t st) {
+              void* workspace, size_t ws_bytes, cudaStream_t st, const RowNorm& norm) {
   return gemm_impl(A, lda, B, ldb, C, ldc, M, N, K, bias, residual, ldr, a_rows_alloc, force_bn, force_splits, 0,
-                   workspace, ws_bytes, st);
+                   workspace, ws_bytes, st, nullptr, norm);
 }
 
 int gemm_swiglu_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int d_ff, int K,
                      int a_rows_alloc, int force_bn, int force_splits, void* workspace, size_t ws_bytes,
-                     cudaStream_t st) {
+                     cudaStream_t st, const RowNorm& norm) {
   return gemm_impl(A, lda, B, ldb, C, ldc, M, 2 * d_ff, K, nullptr, nullptr, 0, a_rows_alloc, force_bn, force_splits,
-                   1, workspace, ws_bytes, st);
+                   1, workspace, ws_bytes, st, nullptr, norm);
 }
 
 int gemm_qkv_rope_bf16(const bf16* A, int lda, const bf16* W, int ldb, const bf16* bias, bf16* qkv, int M, int K,
                        int n_heads, int n_kv, const int* tok_pos, const int* tok_slot, const float* rope,
                        bf16* k_cache, bf16* v_cache, int page_size, int a_rows_alloc, int force_bn,
-                       int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st) {
+                       int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st,
+                       const RowNorm& norm) {
   const int N = (n_heads + 2 * n_kv) * 128;
   QkvRopeArgs qa{tok_pos, tok_slot, rope, k_cache, v_cache, n_heads, n_kv, page_size};
   return gemm_impl(A, lda, W, ldb, qkv, N, M, N, K, bias, nullptr, 0, a_rows_alloc, force_bn, force_splits, 0,
-                   workspace, ws_bytes, st, &qa);
+                   workspace, ws_bytes, st, &qa, norm);
 }
 
 size_t gemm_workspace_bytes(int M, int N, int K) {

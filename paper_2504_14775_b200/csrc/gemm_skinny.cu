@@ -47,15 +47,18 @@ template <int NT, int MODE>
 __device__ __forceinline__ void skinny_epilogue(const float* st, int et, int t, int M, int N, bf16* __restrict__ C,
                                                 int ldc, const bf16* __restrict__ bias,
                                                 const bf16* __restrict__ residual, int ldr,
-                                                const QkvRopeArgs& qa) {
+                                                const QkvRopeArgs& qa, const RowNorm& nm) {
   constexpr int LD = SkSmem<NT>::ST_LD;
+  // fused RMSNorm row scale of token m (1 without a norm)
+  auto row_scale = [&](int m) { return nm.ss_in != nullptr ? rsqrtf(nm.ss_in[m] / nm.d + nm.eps) : 1.f; };
   if constexpr (MODE == EPI_STORE) {
     const int n0 = t * W_ROWS;
     for (int i = et; i < M * 16; i += 128) {
       const int m = i >> 4, c = (i & 15) * 8;
+      const float rs = row_scale(m);
       float v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = st[m * LD + c + j];
+      for (int j = 0; j < 8; ++j) v[j] = st[m * LD + c + j] * rs;
       if (bias != nullptr) {
         const uint4 u = *reinterpret_cast<const uint4*>(bias + n0 + c);
         const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
@@ -80,17 +83,28 @@ __device__ __forceinline__ void skinny_epilogue(const float* st, int et, int t, 
       *reinterpret_cast<uint4*>(C + (size_t)m * ldc + n0 + c) =
           make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
                      pack_bf16x2(v[6], v[7]));
+      if (nm.ss_out != nullptr) {
+        float ss = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float q = bf2f(f2bf(v[j]));
+          ss = fmaf(q, q, ss);
+        }
+        atomicAdd(nm.ss_out + m, ss);
+      }
     }
   } else if constexpr (MODE == EPI_SWIGLU) {
     // W rows interleave 64 gate / 64 up rows: tile t holds gate (f < 64) and up (f >= 64) of
     // output features [64t, 64t + 64); act = bf16(silu(bf16 g)) * bf16(u) as in gemm.cu
     for (int i = et; i < M * 8; i += 128) {
       const int m = i >> 3, c = (i & 7) * 8;
+      const float rs = row_scale(m);
       uint32_t pk[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        float a0 = bf2f(f2bf(st[m * LD + c + 2 * j])), a1 = bf2f(f2bf(st[m * LD + c + 2 * j + 1]));
-        const float b0 = bf2f(f2bf(st[m * LD + 64 + c + 2 * j])), b1 = bf2f(f2bf(st[m * LD + 64 + c + 2 * j + 1]));
+        float a0 = bf2f(f2bf(st[m * LD + c + 2 * j] * rs)), a1 = bf2f(f2bf(st[m * LD + c + 2 * j + 1] * rs));
+        const float b0 = bf2f(f2bf(st[m * LD + 64 + c + 2 * j] * rs)),
+                    b1 = bf2f(f2bf(st[m * LD + 64 + c + 2 * j + 1] * rs));
         a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
         a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
         pk[j] = pack_bf16x2(a0 * b0, a1 * b1);
@@ -106,11 +120,12 @@ __device__ __forceinline__ void skinny_epilogue(const float* st, int et, int t, 
       const int pos = qa.tok_pos[m], slot = qa.tok_slot[m];
       const int page = slot / qa.page_size, off = slot % qa.page_size;
       const float2* cs = reinterpret_cast<const float2*>(qa.rope) + (size_t)pos * 64;
+      const float rs = row_scale(m);
       float a[8], b[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        a[j] = st[m * LD + c + j];
-        b[j] = st[m * LD + 64 + c + j];
+        a[j] = st[m * LD + c + j] * rs;
+        b[j] = st[m * LD + 64 + c + j] * rs;
       }
       if (bias != nullptr) {
 #pragma unroll
@@ -156,7 +171,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, int M,
                     int N, int K, int per, bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
                     const bf16* __restrict__ residual, int ldr, float* __restrict__ partial,
-                    int* __restrict__ counters, const QkvRopeArgs qa) {
+                    int* __restrict__ counters, const QkvRopeArgs qa, const RowNorm nm) {
   using L = SkSmem<NT>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -250,6 +265,8 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
     // epilogue warps 2-5: warp q = w % 4 reads TMEM lanes [32q, 32q + 32) = W rows of the tile
     pdl_wait();  // writes C / partials, reads the residual
     const int q = warp & 3, f = q * 32 + lane, et = threadIdx.x - 64;
+    if (nm.zero != nullptr && blockIdx.x == 0)
+      for (int i = et; i < nm.zero_n; i += 128) nm.zero[i] = 0.f;
     int lt = 0;
     for (int g = g_begin; g < g_end; ++lt) {
       const int t = g / kbs, kb0 = g - t * kbs, nkb = min(kbs - kb0, g_end - g);
@@ -319,7 +336,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
 #pragma unroll
         for (int m = 0; m < NT; ++m) st[m * L::ST_LD + f] = v[m];
         epi_bar();
-        skinny_epilogue<NT, MODE>(st, et, t, M, N, C, ldc, bias, residual, ldr, qa);
+        skinny_epilogue<NT, MODE>(st, et, t, M, N, C, ldc, bias, residual, ldr, qa, nm);
         epi_bar();  // staging is reused by the next tile
       }
     }
@@ -332,7 +349,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
 template <int NT, int MODE>
 int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, int per, int grid, bf16* C,
                   int ldc, const bf16* bias, const bf16* res, int ldr, float* partial, int* counters,
-                  const QkvRopeArgs& qa, cudaStream_t st) {
+                  const QkvRopeArgs& qa, const RowNorm& nm, cudaStream_t st) {
   constexpr int smem = SkSmem<NT>::TOTAL;
   static bool attr = false;
   if (!attr) {
@@ -342,7 +359,7 @@ int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, in
     attr = true;
   }
   cudaError_t e = launch_kernel(gemm_skinny_tcgen05<NT, MODE>, dim3(grid), dim3(THREADS), smem, st, 1, mw, mx, M, N, K,
-                                per, C, ldc, bias, res, ldr, partial, counters, qa);
+                                per, C, ldc, bias, res, ldr, partial, counters, qa, nm);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm_skinny_tcgen05 launch");
   return check_launch("gemm_skinny_tcgen05");
 }
@@ -379,7 +396,7 @@ size_t gemm_skinny_workspace_bytes(int M, int N, int K) {
 
 int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,
                 int K, int mode, const bf16* bias, const bf16* residual, int ldr, const QkvRopeArgs* qkv,
-                void* workspace, size_t ws_bytes, cudaStream_t st) {
+                void* workspace, size_t ws_bytes, cudaStream_t st, const RowNorm& nm) {
   const int nt = M <= 16 ? 16 : 32;
   const size_t need = gemm_skinny_workspace_bytes(M, N, K);
   if (workspace == nullptr || ws_bytes < need)
@@ -402,12 +419,12 @@ int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw
 #define GLLM_SKINNY(NTV)                                                                                     \
   if (mode == EPI_SWIGLU)                                                                                     \
     return launch_skinny<NTV, EPI_SWIGLU>(mw, mx, M, N, K, per, grid, C, ldc, nullptr, nullptr, 0, partial,  \
-                                          counters, qa, st);                                                 \
+                                          counters, qa, nm, st);                                                 \
   if (mode == EPI_QKV_ROPE)                                                                                   \
     return launch_skinny<NTV, EPI_QKV_ROPE>(mw, mx, M, N, K, per, grid, C, ldc, bias, nullptr, 0, partial,   \
-                                            counters, qa, st);                                               \
+                                            counters, qa, nm, st);                                               \
   return launch_skinny<NTV, EPI_STORE>(mw, mx, M, N, K, per, grid, C, ldc, bias, residual, ldr, partial,      \
-                                       counters, qa, st);
+                                       counters, qa, nm, st);
   if (nt == 16) {
     GLLM_SKINNY(16)
   } else {

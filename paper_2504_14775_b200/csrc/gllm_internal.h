@@ -59,20 +59,35 @@ struct QkvRopeArgs {
   int n_heads, n_kv, page_size;
 };
 
+// Fused RMSNorm (gllm_dims.fused_norm): the norm weight is folded into the consumer GEMM's weight
+// columns, the GEMM reads the raw residual stream x, and its epilogue scales output row m by
+// rsqrt(ss_in[m] / d + eps). The producers of x (O / down GEMMs with the residual add) accumulate
+// ss_out[m] += sum of the squares of their bf16 outputs; `zero` (zero_n floats) is cleared by the
+// launch for the next accumulation (one CTA, after the predecessor has finished).
+struct RowNorm {
+  const float* ss_in = nullptr;
+  float* ss_out = nullptr;
+  float* zero = nullptr;
+  int zero_n = 0;
+  int d = 0;
+  float eps = 0.f;
+};
+
 // gemm.cu
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K, const bf16* bias,
               const bf16* residual, int ldr, int a_rows_alloc, int force_bn, int force_splits, void* workspace,
-              size_t ws_bytes, cudaStream_t st);
+              size_t ws_bytes, cudaStream_t st, const RowNorm& norm = RowNorm{});
 // act[M, d_ff] = silu(A W_g^T) * (A W_u^T) with W = the 64-row-interleaved [gate|up] weight [2 d_ff, K]
 int gemm_swiglu_bf16(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int d_ff, int K,
                      int a_rows_alloc, int force_bn, int force_splits, void* workspace, size_t ws_bytes,
-                     cudaStream_t st);
+                     cudaStream_t st, const RowNorm& norm = RowNorm{});
 // qkv = A W^T (+bias) with RoPE on q/k and the k/v heads scattered to the paged cache, fused in
 // the GEMM epilogue (q heads land in qkv rows; k/v columns of qkv are left unwritten)
 int gemm_qkv_rope_bf16(const bf16* A, int lda, const bf16* W, int ldb, const bf16* bias, bf16* qkv, int M, int K,
                        int n_heads, int n_kv, const int* tok_pos, const int* tok_slot, const float* rope,
                        bf16* k_cache, bf16* v_cache, int page_size, int a_rows_alloc, int force_bn,
-                       int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st);
+                       int force_splits, void* workspace, size_t ws_bytes, cudaStream_t st,
+                       const RowNorm& norm = RowNorm{});
 size_t gemm_workspace_bytes(int M, int N, int K);
 
 // gemm_skinny.cu: M <= 32 (decode) GEMMs; mode 0 store (+bias/+residual), 2 SwiGLU, 3 QKV+RoPE+KV write.
@@ -83,7 +98,7 @@ bool gemm_skinny_eligible(int M, int N, int K);
 size_t gemm_skinny_workspace_bytes(int M, int N, int K);
 int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,
                 int K, int mode, const bf16* bias, const bf16* residual, int ldr, const QkvRopeArgs* qkv,
-                void* workspace, size_t ws_bytes, cudaStream_t st);
+                void* workspace, size_t ws_bytes, cudaStream_t st, const RowNorm& norm = RowNorm{});
 int gemm_ws_reset(void* workspace, cudaStream_t st);
 void gemm_ws_mark_clean(const void* workspace);
 // bf16 [rows, cols] (leading dim ld) as a TMA map with 64-col x box_rows boxes, 128B swizzle (cached)
@@ -92,6 +107,8 @@ int make_tma_map_2d(CUtensorMap* out, const void* ptr, int64_t rows, int64_t col
 // kernels.cu
 int rmsnorm(const bf16* x, int ldx, const int* row_index, const bf16* w, bf16* out, int rows, int d, float eps,
             cudaStream_t st);
+// ss[r] = sum over d of x[r][:]^2 (bf16 values), the fused-norm statistics of a stage's input rows
+int row_sumsq(const bf16* x, int ldx, int rows, int d, float* ss, cudaStream_t st);
 int silu_mul(const bf16* gu, int d_ff, bf16* out, int rows, cudaStream_t st);
 int rope_kv_write(bf16* qkv, int n_tokens, int n_heads, int n_kv, int head_dim, const int* tok_pos,
                   const int* tok_slot, const float* rope, bf16* k_cache, bf16* v_cache, int page_size,

@@ -175,6 +175,37 @@ int rmsnorm(const bf16* x, int ldx, const int* row_index, const bf16* w, bf16* o
   return check_launch("rmsnorm");
 }
 
+// ----------------------------------------------------------- fused-norm statistics
+// ss[r] = sum_k x[r][k]^2 over the bf16 values: a warp per row, 16 B loads.
+__global__ void row_sumsq_kernel(const bf16* __restrict__ x, int ldx, int rows, int d, float* __restrict__ ss) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const uint4* xp = reinterpret_cast<const uint4*>(x + (size_t)r * ldx);
+  float acc = 0.f;
+  for (int i = lane; i < d / 8; i += 32) {
+    const uint4 u = xp[i];
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(w4[j]);
+      acc = fmaf(f.x, f.x, acc);
+      acc = fmaf(f.y, f.y, acc);
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) ss[r] = acc;
+}
+
+int row_sumsq(const bf16* x, int ldx, int rows, int d, float* ss, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (d % 8 || ldx % 8) return set_error(GLLM_ERR_INVALID, "row_sumsq needs d, ldx multiples of 8");
+  cudaError_t e = launch_kernel(row_sumsq_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, 1, x, ldx, rows, d, ss);
+  if (e != cudaSuccess) return set_cuda_error(e, "row_sumsq launch");
+  return check_launch("row_sumsq");
+}
+
 // ----------------------------------------------------------- SiLU * mul
 // gu rows hold [gate(d_ff) | up(d_ff)]; out = silu(gate) * up.
 __global__ void silu_mul_kernel(const bf16* __restrict__ gu, int d_ff, bf16* __restrict__ out, size_t groups) {

@@ -144,6 +144,7 @@ struct StageWs {
   size_t gemm_bytes;
   void* attn_part;  // prefill KV-split partials
   size_t attn_part_bytes;
+  float *ss_a, *ss_m;  // fused-norm row statistics (attention / MLP norm inputs)
   size_t total;
 };
 
@@ -178,6 +179,8 @@ static StageWs carve(const gllm_dims& d, uint8_t* base) {
   // heads) and keeps items x kv heads x splits <= 2 x 148 + items x kv heads
   w.attn_part_bytes = attention_split_bytes(4 * 160, 1, 1);
   w.attn_part = take(w.attn_part_bytes);
+  w.ss_a = (float*)take(T * 4);
+  w.ss_m = (float*)take(T * 4);
   w.total = off;
   return w;
 }
@@ -255,20 +258,45 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
       return rc;
 
   const size_t layer_kv = (size_t)d.num_pages * KV * d.page_size * HDIM;
+  // Fused RMSNorm (d.fused_norm): the norm weights live in w_qkv / w_gate_up, the QKV and gate-up
+  // GEMMs read x itself and scale their output rows by rsqrt(mean(x^2) + eps); the O / down GEMMs
+  // accumulate the next norm's sum of squares (ss_m, ss_a) while writing x. The stage input's
+  // statistics come from one row_sumsq pass.
+  const bool fused = d.fused_norm != 0;
+  if (fused)
+    if (int rc = prof_call(P_RMSNORM, 0, 2.0 * Td * Dd, st, [&] { return row_sumsq(x, D, T, D, w.ss_a, st); }))
+      return rc;
+  RowNorm nm_qkv, nm_o, nm_gu, nm_down;
+  if (fused) {
+    nm_qkv.ss_in = w.ss_a;
+    nm_qkv.zero = w.ss_m;
+    nm_qkv.zero_n = T;
+    nm_o.ss_out = w.ss_m;
+    nm_gu.ss_in = w.ss_m;
+    nm_gu.zero = w.ss_a;
+    nm_gu.zero_n = T;
+    nm_down.ss_out = w.ss_a;
+    for (RowNorm* n : {&nm_qkv, &nm_o, &nm_gu, &nm_down}) {
+      n->d = D;
+      n->eps = d.rms_eps;
+    }
+  }
+  const bf16* h_in = fused ? x : w.h;  // A operand of the QKV / gate-up GEMMs
   for (int l = 0; l < d.n_layers; ++l) {
     const gllm_layer& L = S.layers[l];
     bf16* kc = reinterpret_cast<bf16*>(S.k_cache) + (size_t)l * layer_kv;
     bf16* vc = reinterpret_cast<bf16*>(S.v_cache) + (size_t)l * layer_kv;
     int rc;
-    if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
-                        [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.attn_norm, w.h, T, D, d.rms_eps, st); })))
-      return rc;
+    if (!fused)
+      if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
+                          [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.attn_norm, w.h, T, D, d.rms_eps, st); })))
+        return rc;
     // QKV GEMM (+bias) with RoPE and the paged K/V write fused into its epilogue
     if ((rc = prof_call(P_GEMM_QKV, 2.0 * Td * Qd * Dd,
                         gemm_bytes(Td, Qd, Dd, false, L.b_qkv != nullptr) + Td * 2.0 * KV * HDIM * 2.0, st, [&] {
-           return gemm_qkv_rope_bf16(w.h, D, (const bf16*)L.w_qkv, D, (const bf16*)L.b_qkv, w.qkv, T, D, H, KV,
+           return gemm_qkv_rope_bf16(h_in, D, (const bf16*)L.w_qkv, D, (const bf16*)L.b_qkv, w.qkv, T, D, H, KV,
                                      w.tok_pos, w.tok_slot, S.rope, kc, vc, d.page_size, maxT, 0, 0, w.gemm,
-                                     w.gemm_bytes, st);
+                                     w.gemm_bytes, st, nm_qkv);
          })))
       return rc;
     if ((rc = prof_call(P_ATTN, att_flops, att_bytes, st, [&] {
@@ -282,24 +310,25 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
     GLLM_CHECK(w.attn, (size_t)T * H * HDIM, "attention", l);
     if ((rc = prof_call(P_GEMM_O, 2.0 * Td * Dd * Od, gemm_bytes(Td, Dd, Od, true, false), st, [&] {
            return gemm_bf16(w.attn, H * HDIM, (const bf16*)L.w_o, H * HDIM, x, D, T, D, H * HDIM, nullptr, x, D, maxT,
-                            0, 0, w.gemm, w.gemm_bytes, st);
+                            0, 0, w.gemm, w.gemm_bytes, st, nm_o);
          })))
       return rc;
     GLLM_CHECK(x, (size_t)T * D, "gemm_o", l);
-    if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
-                        [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st); })))
-      return rc;
+    if (!fused)
+      if ((rc = prof_call(P_RMSNORM, 0, 4.0 * Td * Dd, st,
+                          [&] { return rmsnorm(x, D, nullptr, (const bf16*)L.mlp_norm, w.h, T, D, d.rms_eps, st); })))
+        return rc;
     // gate-up GEMM with SiLU*mul fused into its epilogue: writes act [T, d_ff] directly
     if ((rc = prof_call(P_GEMM_GU, 2.0 * Td * 2 * Fd * Dd,
                         2.0 * (Td * Dd + 2 * Fd * Dd + Td * Fd), st, [&] {
-           return gemm_swiglu_bf16(w.h, D, (const bf16*)L.w_gate_up, D, w.act, d.d_ff, T, d.d_ff, D, maxT, 0, 0,
-                                   w.gemm, w.gemm_bytes, st);
+           return gemm_swiglu_bf16(h_in, D, (const bf16*)L.w_gate_up, D, w.act, d.d_ff, T, d.d_ff, D, maxT, 0, 0,
+                                   w.gemm, w.gemm_bytes, st, nm_gu);
          })))
       return rc;
     GLLM_CHECK(w.act, (size_t)T * d.d_ff, "gemm_gate_up_swiglu", l);
     if ((rc = prof_call(P_GEMM_DOWN, 2.0 * Td * Dd * Fd, gemm_bytes(Td, Dd, Fd, true, false), st, [&] {
            return gemm_bf16(w.act, d.d_ff, (const bf16*)L.w_down, d.d_ff, x, D, T, D, d.d_ff, nullptr, x, D, maxT, 0,
-                            0, w.gemm, w.gemm_bytes, st);
+                            0, w.gemm, w.gemm_bytes, st, nm_down);
          })))
       return rc;
     GLLM_CHECK(x, (size_t)T * D, "gemm_down", l);

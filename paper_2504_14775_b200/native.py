@@ -33,7 +33,7 @@ class Dims(C.Structure):
                 ("head_dim", C.c_int), ("d_ff", C.c_int), ("vocab", C.c_int), ("qkv_bias", C.c_int),
                 ("rms_eps", C.c_float), ("page_size", C.c_int), ("num_pages", C.c_int), ("max_rows", C.c_int),
                 ("max_pages_per_row", C.c_int), ("max_seq_len", C.c_int), ("max_tokens", C.c_int),
-                ("max_emit", C.c_int)]
+                ("max_emit", C.c_int), ("fused_norm", C.c_int)]
 
 
 class Layer(C.Structure):

@@ -16,6 +16,8 @@ HBM layout per stage (SURVEY §8(d) notation):
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 from dataclasses import dataclass
 
@@ -90,7 +92,7 @@ class StageWorker:
 
     def __init__(self, spec: ModelSpec, layers: range, *, is_first: bool, is_last: bool, num_pages: int,
                  page_size: int, max_rows: int, max_seq_len: int, max_tokens: int, max_emit: int,
-                 seed: int = 0, device="cuda"):
+                 seed: int = 0, device="cuda", fused_norm: bool | None = None):
         import torch
 
         lib = native.load()
@@ -107,8 +109,14 @@ class StageWorker:
         self.q_tile = lib.gllm_attention_q_tile(spec.n_heads, spec.n_kv_heads)
         dev = self.device
         self.layers = [init_layer(spec, l, seed, dev) for l in self.layer_ids]
+        # Fused RMSNorm (include/gllm.h, gllm_dims.fused_norm): fold each norm weight into the columns
+        # of the projection it feeds, W' = W diag(w), and keep unit norm vectors -- the same model
+        # (RMSNorm(x) * w) W^T == RMSNorm(x) W'^T, so the fp32 oracle sees identical math.
+        self.fused_norm = fused_norm if fused_norm is not None else os.environ.get("GLLM_FUSED_NORM", "1") != "0"
         for w in self.layers:   # device layout for the fused SwiGLU epilogue (see include/gllm.h)
             w["w_gate_up"] = interleave_gate_up(w["w_gate_up"], spec.d_ff).contiguous()
+        if self.fused_norm:
+            self._fold_norms()
         self.embed = init_embed(spec, seed, dev, "embed") if is_first else None
         self.final_norm = init_embed(spec, seed, dev, "final_norm") if is_last else None
         self.lm_head = init_embed(spec, seed, dev, "lm_head") if is_last else None
@@ -122,7 +130,7 @@ class StageWorker:
         self.rope = torch.from_numpy(rope_table(spec, max_seq_len)).to(dev)
         self.dims = native.Dims(L, spec.d_model, spec.n_heads, spec.n_kv_heads, spec.head_dim, spec.d_ff, spec.vocab,
                                 int(spec.qkv_bias), spec.rms_eps, page_size, num_pages, max_rows,
-                                self.max_pages_per_row, max_seq_len, max_tokens, max_emit)
+                                self.max_pages_per_row, max_seq_len, max_tokens, max_emit, int(self.fused_norm))
         ws = lib.gllm_stage_workspace_bytes(C.byref(self.dims))
         self.workspace = torch.empty(ws, dtype=torch.uint8, device=dev)
         self._layer_arr = (native.Layer * max(L, 1))()
@@ -133,6 +141,20 @@ class StageWorker:
                                    native.ptr(self.final_norm), native.ptr(self.lm_head), self._layer_arr,
                                    native.ptr(self.k_cache), native.ptr(self.v_cache), native.ptr(self.block_table),
                                    native.ptr(self.token_hist), native.ptr(self.rope), native.ptr(self.workspace), ws)
+
+    def _fold_norms(self) -> None:
+        """W <- W diag(norm), norm <- 1, in place (device pointers unchanged)."""
+        for w in self.layers:
+            for norm, proj in (("attn_norm", "w_qkv"), ("mlp_norm", "w_gate_up")):
+                w[proj].copy_((w[proj].float() * w[norm].float()[None, :]).to(w[proj].dtype))
+                w[norm].fill_(1.0)
+
+    def refold_norms(self) -> None:
+        """Switch to the fused-norm path, folding the current norm weights (tests set non-unit ones)."""
+        self._fold_norms()
+        self.fused_norm = True
+        self.dims.fused_norm = 1
+        self.cstage.dims.fused_norm = 1
 
     def canonical_layers(self) -> list[dict]:
         """Layer weights in the plain [gate; up] layout (for the fp32 oracle)."""

@@ -91,3 +91,49 @@ def test_preemption_on_gpu(cuda_ok):
     for r in reqs:
         # a recompute never re-samples a token that was already generated
         assert len(ex.outputs[r.id]) == r.output_tokens
+
+
+def test_fused_norm_matches_separate_rmsnorm(cuda_ok):
+    """Fused RMSNorm (norm weights folded into w_qkv / w_gate_up, row scales in the GEMM epilogues,
+    statistics accumulated by the O / down epilogues) and separate RMSNorm kernels both stay within
+    2e-2 of the fp32 oracle of the same (unfolded) model, with non-unit norm weights, across
+    prefill + decode micro-batches of the tiny model (2 stages on one GPU)."""
+    import torch
+    from oracle.model_ref import from_stage_workers
+    from paper_2504_14775_b200.executor import LocalExecutor
+    from paper_2504_14775_b200.modelspec import MODELS
+    from paper_2504_14775_b200.stage import StageWorker
+
+    spec = MODELS["tiny"]
+    reqs = [RequestSpec(0, 0.0, 40, 6), RequestSpec(1, 0.5, 75, 5), RequestSpec(2, 2.0, 17, 7)]
+    oracle, worst = None, {}
+    for fused in (False, True):
+        ex = LocalExecutor(spec, reqs, num_pages=64, page_size=16, n_stages=2, max_tokens=256, record_logits=True,
+                           seed=7)
+        g = torch.Generator(device="cpu").manual_seed(11)
+        for i, st in enumerate(ex.stages):
+            new = StageWorker(spec, st.layer_ids, is_first=st.is_first, is_last=st.is_last, num_pages=64,
+                              page_size=16, max_rows=st.max_rows, max_seq_len=st.max_seq_len, max_tokens=256,
+                              max_emit=st.max_emit, seed=7, device=st.device, fused_norm=False)
+            for w in new.layers:
+                for nrm in ("attn_norm", "mlp_norm"):
+                    w[nrm].copy_((0.5 + torch.rand(w[nrm].shape, generator=g)).to(w[nrm].device).bfloat16())
+            ex.stages[i] = new
+        if oracle is None:
+            oracle = from_stage_workers(ex.stages)      # the unfolded model, non-unit norms
+        if fused:
+            for st in ex.stages:
+                st.refold_norms()
+        eng = Engine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(64, 16),
+                     throttle=ThrottleConfig(T=2, min_p=8), executor=ex)
+        eng.run()
+        torch.cuda.synchronize()
+        w_max = 0.0
+        for rid, pos, lg in ex.logits:
+            r = reqs[rid]
+            seq = np.concatenate([prompt_token_ids(rid, r.input_tokens, spec.vocab),
+                                  np.asarray(ex.outputs[rid], dtype=np.int32)])[:pos]
+            want = oracle.logits(seq).numpy()[pos - 1]
+            w_max = max(w_max, float(np.linalg.norm(lg - want) / np.linalg.norm(want)))
+        worst[fused] = w_max
+    assert worst[False] < 2e-2 and worst[True] < 2e-2, worst
