@@ -38,8 +38,6 @@
 namespace gllm {
 
 constexpr int HD = 128;
-constexpr int ATT_THREADS = 128;
-constexpr int NWARP = ATT_THREADS / 32;
 
 // ---------------------------------------------------------------- prefill role
 constexpr int PM = 128;          // query rows per tile (MMA M = TMEM lanes)
@@ -62,14 +60,15 @@ struct PrefillSmem {
 // ---------------------------------------------------------------- decode role
 constexpr int DEC_STAGES = 3;
 constexpr int MAX_PAGE_BYTES = 16 * HD * 2;  // page_size <= 16 for the bulk ring
+template <int NW>  // streaming warps per CTA
 struct DecodeSmem {
   union {
-    __align__(128) uint8_t kv[NWARP][DEC_STAGES][2][MAX_PAGE_BYTES];
-    float merge_acc[NWARP][8][HD];  // reused after every page has been consumed
+    __align__(128) uint8_t kv[NW][DEC_STAGES][2][MAX_PAGE_BYTES];
+    float merge_acc[NW][8][HD];  // reused after every page has been consumed
   };
-  uint64_t full[NWARP][DEC_STAGES];
-  float merge_m[NWARP][8];
-  float merge_l[NWARP][8];
+  uint64_t full[NW][DEC_STAGES];
+  float merge_m[NW][8];
+  float merge_l[NW][8];
 };
 
 
@@ -111,14 +110,14 @@ GLLM_DEVICE void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
 // cp.async.bulk ring and per 16-key page issues 16 HMMA for S = Q.K^T and 16 for
 // O += P.V (P reused from the S accumulator registers), with the online softmax
 // on quads of lanes (one query head per quad). Warps merge through smem.
-template <int G>
+template <int G, int NW>
 __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok, int kv_len,
                                             const int* __restrict__ table, const CUtensorMap* k_map,
                                             const CUtensorMap* v_map, int n_heads, int n_kv, int kvh,
                                             int page_size, float scale_log2, bf16* __restrict__ out) {
   static_assert(G <= 8, "decode tile holds up to 8 query heads per kv head");
   constexpr int HALF_BYTES = 16 * 128;  // one 64-dim box of a 16-slot page (8-slot pages use half)
-  DecodeSmem& sm = *reinterpret_cast<DecodeSmem*>(smem_raw);
+  DecodeSmem<NW>& sm = *reinterpret_cast<DecodeSmem<NW>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qr = lane >> 2;          // fragment row = query head within the group
   const int qc = (lane & 3) * 2;     // fragment column pair
@@ -145,7 +144,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   };
   if (lane == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) {
-      const int p = warp + s * NWARP;
+      const int p = warp + s * NW;
       if (p < n_pages) issue(p, s);
     }
   }
@@ -168,7 +167,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   float m_run = -FLT_MAX, l_run = 0.f;   // row qr's state, replicated across its quad
 
   int it = 0;
-  for (int p = warp; p < n_pages; p += NWARP, ++it) {
+  for (int p = warp; p < n_pages; p += NW, ++it) {
     const int s = it % DEC_STAGES;
     mbar_wait(&sm.full[warp][s], (uint32_t)((it / DEC_STAGES) & 1));
     uint8_t* kp = sm.kv[warp][s][0];
@@ -250,7 +249,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
       mma_16816_bf16(o[nb + 1], a_frag, vb[2], vb[3]);
     }
     __syncwarp();
-    const int pn = p + DEC_STAGES * NWARP;
+    const int pn = p + DEC_STAGES * NW;
     if (lane == 0 && pn < n_pages) {
       fence_proxy_async();
       issue(pn, s);
@@ -271,14 +270,14 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G * HD; i += ATT_THREADS) {
+  for (int i = threadIdx.x; i < G * HD; i += NW * 32) {
     const int h = i / HD, d = i % HD;
     float mx = -FLT_MAX;
 #pragma unroll
-    for (int w = 0; w < NWARP; ++w) mx = fmaxf(mx, sm.merge_m[w][h]);
+    for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm.merge_m[w][h]);
     float num = 0.f, den = 0.f;
 #pragma unroll
-    for (int w = 0; w < NWARP; ++w) {
+    for (int w = 0; w < NW; ++w) {
       const float mw = sm.merge_m[w][h];
       const float c = (mw == -FLT_MAX) ? 0.f : exp2f(mw - mx);
       num += sm.merge_acc[w][h][d] * c;
@@ -717,8 +716,11 @@ attn_split_combine(const int* __restrict__ seq_info, const int* __restrict__ wor
 // A mixed micro-batch is issued as two concurrent launches (prefill items on a forked side
 // stream, decodes on the caller's stream, joined by an event): the prefill kernel takes all of
 // an SM's TMEM and most of its smem, while decode CTAs want two per SM for bytes in flight.
-template <int G>
-__global__ void __launch_bounds__(ATT_THREADS, 2)
+// NW = 4 (two CTAs per SM) for large decode populations; NW = 8 (one CTA, twice the pages in
+// flight per sequence) when the launch has fewer CTAs than two waves: small batches are latency-
+// bound on each sequence's page stream.
+template <int G, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? 2 : 1)
 attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
                    const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
                    const int* __restrict__ block_table, int mpr, int n_heads, int n_kv, int page_size,
@@ -734,8 +736,8 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_const
   const int* si = seq_info + 5 * sidx;
   const int row_id = si[0], start = si[1], tok_off = si[3];
   const int* table = block_table + (size_t)row_id * mpr;
-  decode_role<G>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh, page_size,
-                 scale_log2, out);
+  decode_role<G, NW>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh,
+                     page_size, scale_log2, out);
 }
 
 // Query tokens per prefill work item (a decode, n_new == 1, is always one item).
@@ -756,15 +758,20 @@ template <bool PREFILL, int G>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
                        int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
                        float scale_log2, bf16* out, cudaStream_t st, const AttnSplit& sp = AttnSplit{}) {
-  constexpr size_t smem = (PREFILL ? sizeof(PrefillSmem) : sizeof(DecodeSmem)) + 1024;
+  constexpr size_t smem_pf = sizeof(PrefillSmem) + 1024;
+  constexpr size_t smem4 = sizeof(DecodeSmem<4>) + 1024, smem8 = sizeof(DecodeSmem<8>) + 1024;
   static bool attr = false;
   if (!attr) {
-    const void* fn = PREFILL ? (const void*)attn_prefill_kernel<G> : (const void*)attn_decode_kernel<G>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "attention smem attribute");
-    // all of the unified L1/smem as shared memory (decode: two CTAs, 8 streaming warps per SM)
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return set_cuda_error(e, "attention carveout attribute");
+    const void* fns[3] = {(const void*)attn_prefill_kernel<G>, (const void*)attn_decode_kernel<G, 4>,
+                          (const void*)attn_decode_kernel<G, 8>};
+    const size_t sm[3] = {smem_pf, smem4, smem8};
+    for (int i = PREFILL ? 0 : 1; i < (PREFILL ? 1 : 3); ++i) {
+      cudaError_t e = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm[i]);
+      if (e != cudaSuccess) return set_cuda_error(e, "attention smem attribute");
+      // all of the unified L1/smem as shared memory (decode: 8 streaming warps per SM)
+      e = cudaFuncSetAttribute(fns[i], cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return set_cuda_error(e, "attention carveout attribute");
+    }
     attr = true;
   }
   // the paged cache viewed as a 2-D [pages*kv_heads*page_size, 128] bf16 tensor: one TMA box per
@@ -775,7 +782,7 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
   dim3 grid(n_kv, n_work);
   if constexpr (PREFILL) {
     grid.y = n_work * sp.n_split;
-    attn_prefill_kernel<G><<<grid, PF_THREADS, smem, st>>>(km, vm, qkv, seq_info, work, n_work, block_table, mpr,
+    attn_prefill_kernel<G><<<grid, PF_THREADS, smem_pf, st>>>(km, vm, qkv, seq_info, work, n_work, block_table, mpr,
                                                             n_heads, n_kv, page_size, scale_log2, out, sp.n_split,
                                                             sp.part_o, sp.part_ml);
     if (int rc = check_launch("attention_prefill")) return rc;
@@ -786,8 +793,11 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
     }
     return 0;
   } else {
-    cudaError_t e = launch_kernel(attn_decode_kernel<G>, grid, dim3(ATT_THREADS), smem, st, 1, km, vm, qkv, seq_info,
-                                  work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out);
+    const bool wide = (long)n_work * n_kv < 2L * device_sm_count();
+    cudaError_t e = wide ? launch_kernel(attn_decode_kernel<G, 8>, grid, dim3(256), smem8, st, 1, km, vm, qkv, seq_info,
+                                         work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out)
+                         : launch_kernel(attn_decode_kernel<G, 4>, grid, dim3(128), smem4, st, 1, km, vm, qkv, seq_info,
+                                         work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out);
     if (e != cudaSuccess) return set_cuda_error(e, "attention_decode launch");
     return check_launch("attention_decode");
   }
