@@ -294,20 +294,6 @@ GLLM_DEVICE float ex2_approx(float x) {
   return y;
 }
 
-// 2^x on the FMA pipe (offloads the MUFU unit, which the softmax otherwise saturates):
-// n = rint(x) by the 1.5*2^23 trick, 2^(x-n) with x-n in [-0.5, 0.5] by a degree-3 polynomial
-// (max relative error 1.0e-4, well under bf16's 2^-9 rounding of P), 2^n added to the exponent.
-GLLM_DEVICE float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float t = x + 12582912.f;
-  const float f = x - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05500871f, f, 0.24221069f), f, 0.6932829f), f, 1.f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-#ifndef GLLM_EXP2_EMU
-#define GLLM_EXP2_EMU 0   // of every 4 P pairs, this many are exponentiated on the FMA pipe
-#endif
-
 // Packed fp32 pairs (FFMA2 / FADD2 on sm_100): half the issue slots of scalar FFMA / FADD.
 GLLM_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
   float2 d;
@@ -341,14 +327,7 @@ GLLM_DEVICE void softmax_p_half(uint32_t t_s, int h, float2 sc2, float2 ng2, int
   for (int e = 0; e < 32; ++e) {
     const uint32_t* sv = e < 16 ? s0 : s1;
     const float2 x = ffma2(make_float2(__uint_as_float(sv[(2 * e) & 31]), __uint_as_float(sv[(2 * e + 1) & 31])), sc2, ng2);
-    float a, b;
-    if ((e & 3) < GLLM_EXP2_EMU) {
-      a = ex2_poly(x.x);
-      b = ex2_poly(x.y);
-    } else {
-      a = ex2_approx(x.x);
-      b = ex2_approx(x.y);
-    }
+    float a = ex2_approx(x.x), b = ex2_approx(x.y);
     if constexpr (DIAG) {
       const int c = h * 64 + 2 * e;
       a = c <= kmax ? a : 0.f;

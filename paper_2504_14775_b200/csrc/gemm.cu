@@ -47,7 +47,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
                                               float* __restrict__ partial, const QkvRopeArgs& qa,
                                               const RowNorm& nm) {
   // fused RMSNorm: this row's scale for the GEMM output (ss_in), and its output statistics (ss_out)
-  const float rs = (nm.ss_in != nullptr && row < M) ? rsqrtf(nm.ss_in[row] / nm.d + nm.eps) : 1.f;
+  const float rs = (nm.ss_in != nullptr && row < M) ? row_norm_scale(nm, row) : 1.f;
   if constexpr (MODE == EPI_QKV_ROPE) {
     // Head-aligned tile: columns [128h, 128h+128) are one whole head of this token row, so the
     // rotate-half pairs (d, d+64) are thread-local. q heads are rotated and written back to C;
@@ -198,10 +198,13 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
             const float q = bf2f(f2bf(v[j]));
             ss = fmaf(q, q, ss);
           }
+          if (c & 32) {  // end of a 64-column group
+            nm.ss_out[(size_t)((col & ~(NORM_GROUP - 1)) / NORM_GROUP) * nm.ld + row] = ss;
+            ss = 0.f;
+          }
         }
       }
     }
-    if (nm.ss_out != nullptr && row < M) atomicAdd(nm.ss_out + row, ss);
   }
 }
 
@@ -345,8 +348,6 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
   } else {
     // Epilogue warps 2-5: warp (w % 4) may only touch TMEM lanes [32*(w%4), 32*(w%4)+32).
     pdl_wait();  // C / residual / KV cache are shared with the predecessor
-    if (nm.zero != nullptr && blockIdx.x == 0)
-      for (int i = threadIdx.x - 64; i < nm.zero_n; i += 128) nm.zero[i] = 0.f;
     const int q = warp & 3;
     const uint32_t acc_empty_leader = CG == 2 ? mapa_shared(smem_u32(acc_empty), 0) : 0u;
     int lt = 0;
@@ -379,7 +380,14 @@ __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int
                               const RowNorm nm) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t groups = (size_t)M * (N / 8);
-  if (idx >= groups) return;
+  // (lanes past the end stay for the column-group shuffle below; M * N / 8 is a multiple of 8)
+  if (idx >= groups) {
+    if (nm.ss_out != nullptr) {
+      float z = 0.f;
+      for (int o = 1; o < 8; o <<= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    }
+    return;
+  }
   const int row = (int)(idx / (N / 8));
   const int col = (int)(idx % (N / 8)) * 8;
   float v[8];
@@ -394,7 +402,7 @@ __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int
     v[0] += a.x; v[1] += a.y; v[2] += a.z; v[3] += a.w; v[4] += b.x; v[5] += b.y; v[6] += b.z; v[7] += b.w;
   }
   if (nm.ss_in != nullptr) {
-    const float rs = rsqrtf(nm.ss_in[row] / nm.d + nm.eps);
+    const float rs = row_norm_scale(nm, row);
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] *= rs;
   }
@@ -421,13 +429,15 @@ __global__ void splitk_reduce(const float* __restrict__ partial, int splits, int
   *reinterpret_cast<uint4*>(C + (size_t)row * ldc + col) =
       make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
   if (nm.ss_out != nullptr) {
+    // the 8 consecutive lanes of a 64-column group reduce in a fixed butterfly order
     float ss = 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float q = bf2f(f2bf(v[j]));
       ss = fmaf(q, q, ss);
     }
-    atomicAdd(nm.ss_out + row, ss);
+    for (int o = 1; o < 8; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((col & (NORM_GROUP - 1)) == 0) nm.ss_out[(size_t)(col / NORM_GROUP) * nm.ld + row] = ss;
   }
 }
 
@@ -452,7 +462,7 @@ __global__ void splitk_reduce_swiglu(const float* __restrict__ partial, int spli
       u[j] += base[gcol + 64 + j];
     }
   }
-  const float rs = nm.ss_in != nullptr ? rsqrtf(nm.ss_in[row] / nm.d + nm.eps) : 1.f;
+  const float rs = nm.ss_in != nullptr ? row_norm_scale(nm, row) : 1.f;
   uint32_t pk[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {

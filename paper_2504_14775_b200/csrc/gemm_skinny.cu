@@ -36,7 +36,8 @@ struct SkSmem {
   static constexpr int ST_LD = W_ROWS + 4;  // fp32 transpose staging [NT][ST_LD]
   static constexpr int STAGE_OFF = 0;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
-  static constexpr int BAR_OFF = EPI_OFF + NT * ST_LD * 4;
+  static constexpr int RS_OFF = EPI_OFF + NT * ST_LD * 4;  // fused-norm row scales [NT]
+  static constexpr int BAR_OFF = RS_OFF + NT * 4;
   static constexpr int TOTAL = 1024 + BAR_OFF + 256;
 };
 
@@ -47,50 +48,57 @@ template <int NT, int MODE>
 __device__ __forceinline__ void skinny_epilogue(const float* st, int et, int t, int M, int N, bf16* __restrict__ C,
                                                 int ldc, const bf16* __restrict__ bias,
                                                 const bf16* __restrict__ residual, int ldr,
-                                                const QkvRopeArgs& qa, const RowNorm& nm) {
+                                                const QkvRopeArgs& qa, const RowNorm& nm, const float* rs_sm) {
   constexpr int LD = SkSmem<NT>::ST_LD;
-  // fused RMSNorm row scale of token m (1 without a norm)
-  auto row_scale = [&](int m) { return nm.ss_in != nullptr ? rsqrtf(nm.ss_in[m] / nm.d + nm.eps) : 1.f; };
+  // fused RMSNorm row scale of token m (1 without a norm), precomputed in smem by the caller
+  auto row_scale = [&](int m) { return nm.ss_in != nullptr ? rs_sm[m] : 1.f; };
   if constexpr (MODE == EPI_STORE) {
     const int n0 = t * W_ROWS;
-    for (int i = et; i < M * 16; i += 128) {
-      const int m = i >> 4, c = (i & 15) * 8;
-      const float rs = row_scale(m);
-      float v[8];
+    // every lane runs the same trip count: 8 consecutive lanes = one 64-column group of a row,
+    // reduced by a fixed butterfly for the fused-norm statistics
+    for (int base = 0; base < M * 16; base += 128) {
+      const int i = base + et;
+      const bool live = i < M * 16;
+      const int m = live ? i >> 4 : 0, c = (i & 15) * 8;
+      float sq = 0.f;
+      if (live) {
+        const float rs = row_scale(m);
+        float v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = st[m * LD + c + j] * rs;
-      if (bias != nullptr) {
-        const uint4 u = *reinterpret_cast<const uint4*>(bias + n0 + c);
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        for (int j = 0; j < 8; ++j) v[j] = st[m * LD + c + j] * rs;
+        if (bias != nullptr) {
+          const uint4 u = *reinterpret_cast<const uint4*>(bias + n0 + c);
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16x2(w4[j]);
-          v[2 * j] += f.x;
-          v[2 * j + 1] += f.y;
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(w4[j]);
+            v[2 * j] += f.x;
+            v[2 * j + 1] += f.y;
+          }
         }
-      }
-      if (residual != nullptr) {
-        // round the GEMM result to bf16 first, then add: same as bf16 "x + attn(x)"
-        const uint4 u = *reinterpret_cast<const uint4*>(residual + (size_t)m * ldr + n0 + c);
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+        if (residual != nullptr) {
+          // round the GEMM result to bf16 first, then add: same as bf16 "x + attn(x)"
+          const uint4 u = *reinterpret_cast<const uint4*>(residual + (size_t)m * ldr + n0 + c);
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = unpack_bf16x2(w4[j]);
-          v[2 * j] = bf2f(f2bf(v[2 * j])) + f.x;
-          v[2 * j + 1] = bf2f(f2bf(v[2 * j + 1])) + f.y;
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack_bf16x2(w4[j]);
+            v[2 * j] = bf2f(f2bf(v[2 * j])) + f.x;
+            v[2 * j + 1] = bf2f(f2bf(v[2 * j + 1])) + f.y;
+          }
         }
-      }
-      *reinterpret_cast<uint4*>(C + (size_t)m * ldc + n0 + c) =
-          make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
-                     pack_bf16x2(v[6], v[7]));
-      if (nm.ss_out != nullptr) {
-        float ss = 0.f;
+        *reinterpret_cast<uint4*>(C + (size_t)m * ldc + n0 + c) =
+            make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                       pack_bf16x2(v[6], v[7]));
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const float q = bf2f(f2bf(v[j]));
-          ss = fmaf(q, q, ss);
+          sq = fmaf(q, q, sq);
         }
-        atomicAdd(nm.ss_out + m, ss);
+      }
+      if (nm.ss_out != nullptr) {
+        for (int o = 1; o < 8; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (live && (c & (NORM_GROUP - 1)) == 0) nm.ss_out[(size_t)((n0 + c) / NORM_GROUP) * nm.ld + m] = sq;
       }
     }
   } else if constexpr (MODE == EPI_SWIGLU) {
@@ -177,6 +185,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* st = reinterpret_cast<float*>(smem + L::EPI_OFF);
+  float* rs_sm = reinterpret_cast<float*>(smem + L::RS_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
@@ -265,8 +274,10 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
     // epilogue warps 2-5: warp q = w % 4 reads TMEM lanes [32q, 32q + 32) = W rows of the tile
     pdl_wait();  // writes C / partials, reads the residual
     const int q = warp & 3, f = q * 32 + lane, et = threadIdx.x - 64;
-    if (nm.zero != nullptr && blockIdx.x == 0)
-      for (int i = et; i < nm.zero_n; i += 128) nm.zero[i] = 0.f;
+    if (nm.ss_in != nullptr) {
+      if (et < M) rs_sm[et] = row_norm_scale(nm, et);
+      epi_bar();
+    }
     int lt = 0;
     for (int g = g_begin; g < g_end; ++lt) {
       const int t = g / kbs, kb0 = g - t * kbs, nkb = min(kbs - kb0, g_end - g);
@@ -336,7 +347,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
 #pragma unroll
         for (int m = 0; m < NT; ++m) st[m * L::ST_LD + f] = v[m];
         epi_bar();
-        skinny_epilogue<NT, MODE>(st, et, t, M, N, C, ldc, bias, residual, ldr, qa, nm);
+        skinny_epilogue<NT, MODE>(st, et, t, M, N, C, ldc, bias, residual, ldr, qa, nm, rs_sm);
         epi_bar();  // staging is reused by the next tile
       }
     }

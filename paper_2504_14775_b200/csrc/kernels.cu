@@ -176,32 +176,34 @@ int rmsnorm(const bf16* x, int ldx, const int* row_index, const bf16* w, bf16* o
 }
 
 // ----------------------------------------------------------- fused-norm statistics
-// ss[r] = sum_k x[r][k]^2 over the bf16 values: a warp per row, 16 B loads.
-__global__ void row_sumsq_kernel(const bf16* __restrict__ x, int ldx, int rows, int d, float* __restrict__ ss) {
+// ss[g][r] = sum of x[r][64g .. 64g+64)^2 over the bf16 values (the layout the O / down GEMM
+// epilogues write): a warp per row, lane = 8 columns, 8 lanes per group reduced by a butterfly.
+__global__ void row_sumsq_kernel(const bf16* __restrict__ x, int ldx, int rows, int d, float* __restrict__ ss,
+                                 int ld) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (r >= rows) return;
+  if (r >= rows) return;  // whole warps
   const uint4* xp = reinterpret_cast<const uint4*>(x + (size_t)r * ldx);
-  float acc = 0.f;
   for (int i = lane; i < d / 8; i += 32) {
     const uint4 u = xp[i];
     const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+    float acc = 0.f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 f = unpack_bf16x2(w4[j]);
       acc = fmaf(f.x, f.x, acc);
       acc = fmaf(f.y, f.y, acc);
     }
+    for (int o = 1; o < 8; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((i & 7) == 0) ss[(size_t)(i / 8) * ld + r] = acc;
   }
-  acc = warp_sum(acc);
-  if (lane == 0) ss[r] = acc;
 }
 
-int row_sumsq(const bf16* x, int ldx, int rows, int d, float* ss, cudaStream_t st) {
+int row_sumsq(const bf16* x, int ldx, int rows, int d, float* ss, int ld, cudaStream_t st) {
   if (rows <= 0) return 0;
-  if (d % 8 || ldx % 8) return set_error(GLLM_ERR_INVALID, "row_sumsq needs d, ldx multiples of 8");
-  cudaError_t e = launch_kernel(row_sumsq_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, 1, x, ldx, rows, d, ss);
+  if (d % 256 || ldx % 8) return set_error(GLLM_ERR_INVALID, "row_sumsq needs d %% 256 == 0 and ldx %% 8 == 0");
+  cudaError_t e = launch_kernel(row_sumsq_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, 1, x, ldx, rows, d, ss, ld);
   if (e != cudaSuccess) return set_cuda_error(e, "row_sumsq launch");
   return check_launch("row_sumsq");
 }

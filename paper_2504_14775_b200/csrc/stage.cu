@@ -179,8 +179,8 @@ static StageWs carve(const gllm_dims& d, uint8_t* base) {
   // heads) and keeps items x kv heads x splits <= 2 x 148 + items x kv heads
   w.attn_part_bytes = attention_split_bytes(4 * 160, 1, 1);
   w.attn_part = take(w.attn_part_bytes);
-  w.ss_a = (float*)take(T * 4);
-  w.ss_m = (float*)take(T * 4);
+  w.ss_a = (float*)take(T * (d.d_model / NORM_GROUP) * 4);
+  w.ss_m = (float*)take(T * (d.d_model / NORM_GROUP) * 4);
   w.total = off;
   return w;
 }
@@ -260,23 +260,21 @@ static int forward(const gllm_stage& S, const gllm_batch& B, cudaStream_t st) {
   const size_t layer_kv = (size_t)d.num_pages * KV * d.page_size * HDIM;
   // Fused RMSNorm (d.fused_norm): the norm weights live in w_qkv / w_gate_up, the QKV and gate-up
   // GEMMs read x itself and scale their output rows by rsqrt(mean(x^2) + eps); the O / down GEMMs
-  // accumulate the next norm's sum of squares (ss_m, ss_a) while writing x. The stage input's
-  // statistics come from one row_sumsq pass.
+  // write the next norm's per-64-column sums of squares (ss_m, ss_a) while writing x. The stage
+  // input's statistics come from one row_sumsq pass.
   const bool fused = d.fused_norm != 0;
+  if (fused && D % 256) return set_error(GLLM_ERR_INVALID, "fused_norm needs d_model %% 256 == 0");
   if (fused)
-    if (int rc = prof_call(P_RMSNORM, 0, 2.0 * Td * Dd, st, [&] { return row_sumsq(x, D, T, D, w.ss_a, st); }))
+    if (int rc = prof_call(P_RMSNORM, 0, 2.0 * Td * Dd, st, [&] { return row_sumsq(x, D, T, D, w.ss_a, maxT, st); }))
       return rc;
   RowNorm nm_qkv, nm_o, nm_gu, nm_down;
   if (fused) {
     nm_qkv.ss_in = w.ss_a;
-    nm_qkv.zero = w.ss_m;
-    nm_qkv.zero_n = T;
     nm_o.ss_out = w.ss_m;
     nm_gu.ss_in = w.ss_m;
-    nm_gu.zero = w.ss_a;
-    nm_gu.zero_n = T;
     nm_down.ss_out = w.ss_a;
     for (RowNorm* n : {&nm_qkv, &nm_o, &nm_gu, &nm_down}) {
+      n->ld = maxT;
       n->d = D;
       n->eps = d.rms_eps;
     }

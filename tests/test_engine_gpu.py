@@ -137,3 +137,24 @@ def test_fused_norm_matches_separate_rmsnorm(cuda_ok):
             w_max = max(w_max, float(np.linalg.norm(lg - want) / np.linalg.norm(want)))
         worst[fused] = w_max
     assert worst[False] < 2e-2 and worst[True] < 2e-2, worst
+
+
+def test_pdl_bit_identical(cuda_ok):
+    """Programmatic dependent launch lets kernels start before their predecessor finishes; every
+    kernel must wait (griddepcontrol.wait) before touching shared memory. A missed wait is a race:
+    the served tokens and logits must be bit-identical with PDL on and off."""
+    import json
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for pdl in ("1", "0"):
+        env = dict(os.environ, GLLM_PDL=pdl)
+        r = subprocess.run([sys.executable, os.path.join(here, "pdl_equivalence_run.py")], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0]["launches"] > 10
+    assert outs[0]["tokens"] == outs[1]["tokens"]
+    assert outs[0]["logits_sha256"] == outs[1]["logits_sha256"]
