@@ -696,8 +696,8 @@ attn_split_combine(const int* __restrict__ seq_info, const int* __restrict__ wor
 // stream, decodes on the caller's stream, joined by an event): the prefill kernel takes all of
 // an SM's TMEM and most of its smem, while decode CTAs want two per SM for bytes in flight.
 // NW = 4 (two CTAs per SM) for large decode populations; NW = 8 (one CTA, twice the pages in
-// flight per sequence) when the launch has fewer CTAs than two waves: small batches are latency-
-// bound on each sequence's page stream.
+// flight per sequence) when all (sequence, kv head) items fit in one wave of SMs: small batches
+// are latency-bound on each sequence's page stream.
 template <int G, int NW>
 __global__ void __launch_bounds__(NW * 32, NW == 4 ? 2 : 1)
 attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
@@ -772,7 +772,7 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
     }
     return 0;
   } else {
-    const bool wide = (long)n_work * n_kv < 2L * device_sm_count();
+    const bool wide = (long)n_work * n_kv <= device_sm_count();  // one wave of 8-warp CTAs
     cudaError_t e = wide ? launch_kernel(attn_decode_kernel<G, 8>, grid, dim3(256), smem8, st, 1, km, vm, qkv, seq_info,
                                          work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out)
                          : launch_kernel(attn_decode_kernel<G, 4>, grid, dim3(128), smem4, st, 1, km, vm, qkv, seq_info,
