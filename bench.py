@@ -148,6 +148,10 @@ def roofline(profile: dict, peaks: dict) -> dict:
             traffic_src = f"profiles/ncu_traffic.json ({t['shape']})"
     except OSError:
         pass
+    # both resources at once: a class mixing bandwidth- and compute-bound work (the attention call
+    # runs decode and prefill launches concurrently) is judged against bytes/HBM + FLOPs/tensor
+    t_ideal = e["bytes"] / (peaks["hbm_gbs"] * 1e9) + e["flops"] / (peaks["bf16_tflops_sustained"] * 1e12)
+    out["frac_bytes_plus_flops"] = round(t_ideal / (e["total_ms"] * 1e-3), 4)
     out.update({"kernel": name, "achieved": round(achieved, 2), "peak": peak, "frac": round(achieved / peak, 4),
                 "traffic": traffic, "traffic_src": traffic_src, "launches": e["launches"],
                 "avg_launch_ms": round(per_launch_ms, 4),
