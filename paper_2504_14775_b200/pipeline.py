@@ -428,6 +428,16 @@ class _HostEvent:
 # ------------------------------------------------------------------ bench entry (torchrun, N > 1)
 
 
+def _bubble(busy) -> float:
+    """Idle fraction of one stage between its first start and last end (CUDA-event busy intervals;
+    the reference's per-stage bubble definition, `engine.py:108-125`, over the measured run)."""
+    if not busy:
+        return 0.0
+    t0 = min(a for a, _ in busy)
+    t1 = max(b for _, b in busy)
+    return 1.0 - sum(b - a for a, b in busy) / max(t1 - t0, 1e-9)
+
+
 def bench_pipeline(args) -> int:
     """`bench.py --gpus N` under torchrun: PP=N over the same model and trace (strong scaling)."""
     import json
@@ -479,9 +489,13 @@ def bench_pipeline(args) -> int:
         out = worker_loop(spec, reqs, rank=rank, world=world, meta=meta, transport=transport, num_pages=num_pages,
                           page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests,
                           device=f"cuda:{dev_id}")
-        stats = torch.tensor([0.0, float(native.launch_count() - launches0), float(out["batches"])],
+        # per-batch launches of this stage (the timed window is only known to rank 0)
+        stats = torch.tensor([0.0, (native.launch_count() - launches0) / max(out["batches"], 1), 0.0],
                              dtype=torch.float64)
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=gloo)
+        bub = torch.zeros(world, dtype=torch.float64)
+        bub[rank] = _bubble(out["busy"])
+        dist.all_reduce(bub, op=dist.ReduceOp.SUM, group=gloo)
         dist.destroy_process_group()
         return 0
     ex = PipelineExecutor(spec, reqs, world=world, meta=meta, transport=transport, num_pages=num_pages,
@@ -521,9 +535,12 @@ def bench_pipeline(args) -> int:
     ex.shutdown()
     # rank 0's driver clock spans every stage of every timed batch (a batch commits only after
     # the last rank's tokens arrive), so it is the max over ranks of the pipeline's time.
-    stats = torch.tensor([st["t1"] - st["t0"], float(native.launch_count() - launches0), float(ex.launches)],
+    stats = torch.tensor([st["t1"] - st["t0"], (native.launch_count() - launches0) / max(ex.launches, 1), 0.0],
                          dtype=torch.float64)
     dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=gloo)
+    bub = torch.zeros(world, dtype=torch.float64)
+    bub[0] = _bubble(ex.stage_busy_intervals()[0])
+    dist.all_reduce(bub, op=dist.ReduceOp.SUM, group=gloo)
     wall = stats[0:1]
     out_tok = sum(n for _, _, n in st["timed"])
     raw = eng.raw_data()
@@ -537,9 +554,11 @@ def bench_pipeline(args) -> int:
             "e2e": {"value": round(out_tok / wall.item(), 2), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(ex.h2d_bytes_total_for([s for s, _, _ in st["timed"]]) / max(K, 1)),
                     "d2h_bytes_per_step": int(4 * out_tok / max(K, 1))},
-            "gpu_launches": int(stats[1].item()), "clocks": clk,
+            "gpu_launches": int(round(stats[1].item() * K)),  # sum over stages of launches per batch x K
+            "clocks": clk,
             "transport": "host-staged gloo (test)" if host_transport else "nccl p2p",
             "serving": {"p50_ttft_ms": rep.ttft_p50_ms, "p50_tpot_ms": rep.tpot_p50_ms,
+                        "bubble_frac_per_stage": [round(float(b), 4) for b in bub.tolist()],
                         "decodes_per_step": statistics.mean(eng._iters[s].decode_tokens for s, _, _ in st["timed"])}}
     print(json.dumps(line))
     dist.destroy_process_group()
