@@ -153,6 +153,10 @@ GLLM_API int gllm_commit_tokens(const gllm_stage* stage, const gllm_batch* batch
  * (16 KB) holds tile counters that must be zero between calls; these entry points zero them
  * themselves (gllm_stage_forward once per forward). workspace >= 16 KB + 42 MB covers every
  * shape a stage issues. */
+/* Zero the workspace head once and let the following GEMM calls on this host thread that pass
+ * the same workspace skip their own zeroing (every launch leaves the counters zero): for chains
+ * of individual GEMMs. The caller must not write the workspace between those calls. */
+GLLM_API int gllm_gemm_workspace_reset(void* workspace, gllm_stream_t stream);
 GLLM_API int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N, int K,
                    const void* bias, const void* residual, int ldr, int force_bn, int force_splits,
                    void* workspace, size_t workspace_bytes, gllm_stream_t stream);

@@ -1,6 +1,7 @@
 """Build libgllm.so (sm_100a) in-tree with nvcc.
 
-    python -m paper_2504_14775_b200.build [--force]
+    python -m paper_2504_14775_b200.build [--force] [-v]
+    python -m paper_2504_14775_b200.build --define GLLM_TRACE --out old_lib/libgllm_trace.so   # debug variant
 
 The shared library links the CUDA runtime statically and resolves the driver
 API (cuTensorMapEncodeTiled) at run time, so it loads on a CPU-only host (the
@@ -36,29 +37,32 @@ def flags() -> list[str]:
             "-I", os.path.join(ROOT, "include"), "-DNDEBUG"]
 
 
-def _digest() -> str:
+def _digest(extra: list[str]) -> str:
     h = hashlib.sha256()
     for name in SOURCES + HEADERS:
         with open(os.path.join(CSRC, name), "rb") as fh:
             h.update(fh.read())
     with open(os.path.join(ROOT, "include", "gllm.h"), "rb") as fh:
         h.update(fh.read())
-    h.update(" ".join(flags()).encode())
+    h.update(" ".join(flags() + extra).encode())
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stamp = LIB + ".sha256"
-    dg = _digest()
-    if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read().strip() == dg:
-        return LIB
-    objdir = os.path.join(PKG, "build")
+def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (), out: str | None = None) -> str:
+    """Build the library; `defines` / `out` make a debug variant (e.g. GLLM_TRACE) at another path."""
+    lib = os.path.abspath(out) if out else LIB
+    extra = [f"-D{d}" for d in defines]
+    stamp = lib + ".sha256"
+    dg = _digest(extra)
+    if not force and os.path.exists(lib) and os.path.exists(stamp) and open(stamp).read().strip() == dg:
+        return lib
+    objdir = os.path.join(PKG, "build" if not defines else "build_" + "_".join(defines).lower())
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for name in SOURCES:
         obj = os.path.join(objdir, name.replace(".cu", ".o"))
-        cmd = [nvcc(), *flags(), "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, name), "-o", obj]
+        cmd = [nvcc(), *flags(), *extra, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, name), "-o", obj]
         procs.append((name, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
     failed = []
@@ -74,14 +78,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     vscript = os.path.join(objdir, "exports.map")
     with open(vscript, "w") as fh:
         fh.write("{ global: gllm_*; local: *; };\n")
-    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", LIB + ".tmp",
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", lib + ".tmp",
             "-Xlinker", f"--version-script={vscript}", "-cudart", "static"]
     subprocess.run(link, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     with open(stamp, "w") as fh:
         fh.write(dg + "\n")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--define", action="append", default=[])
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, defines=tuple(a.define), out=a.out))

@@ -29,7 +29,7 @@ constexpr int EPI_STORE = 0, EPI_SWIGLU = 2, EPI_QKV_ROPE = 3;
 
 template <int NT>
 struct SkSmem {
-  static constexpr int STAGES = 8;
+  static constexpr int STAGES = 8;  // 11 (more weights prefetched ahead of the PDL wait) measured neutral
   static constexpr int W_BYTES = W_ROWS * KB * 2;
   static constexpr int X_BYTES = NT * KB * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
@@ -40,6 +40,21 @@ struct SkSmem {
   static constexpr int BAR_OFF = RS_OFF + NT * 4;
   static constexpr int TOTAL = 1024 + BAR_OFF + 256;
 };
+
+// Debug builds (-DGLLM_TRACE, tools/skinny_trace.py): %globaltimer stamps of each CTA's phases
+// in a ring of TRACE_LAUNCHES launches, read back with gllm_debug_trace_read.
+#ifdef GLLM_TRACE
+constexpr int TRACE_LAUNCHES = 64, TRACE_CTAS = 160, TRACE_EV = 12;
+__device__ unsigned long long g_trace[TRACE_LAUNCHES][TRACE_CTAS][TRACE_EV];
+__device__ __forceinline__ void trace(int tag, int ev) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (blockIdx.x < TRACE_CTAS) g_trace[tag % TRACE_LAUNCHES][blockIdx.x][ev] = t;
+}
+#define SK_TRACE(ev) trace(tag, ev)
+#else
+#define SK_TRACE(ev) ((void)tag)
+#endif
 
 GLLM_DEVICE void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -179,7 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, int M,
                     int N, int K, int per, bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
                     const bf16* __restrict__ residual, int ldr, float* __restrict__ partial,
-                    int* __restrict__ counters, const QkvRopeArgs qa, const RowNorm nm) {
+                    int* __restrict__ counters, const QkvRopeArgs qa, const RowNorm nm, int tag) {
   using L = SkSmem<NT>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -194,6 +209,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
   volatile uint32_t* last_flag = tmem_slot + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SK_TRACE(0);
   pdl_trigger();
   const int kbs = K / KB;
   const int work = (N / W_ROWS) * kbs;
@@ -217,6 +233,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) SK_TRACE(1);
 
   if (warp == 0) {
     if (elect_one()) {
@@ -232,6 +249,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
         tma_load_2d_hint(&map_w, &full[i], smem + i * L::STAGE_BYTES, (g - t * kbs) * KB, t * W_ROWS, pol_w);
       }
       pdl_wait();
+      SK_TRACE(2);
       for (int i = 0; i < n_it; ++i) {
         const int g = g_begin + i, t = g / kbs, kc = (g - t * kbs) * KB;
         const int s = i % STAGES;
@@ -257,6 +275,10 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         tc_fence_after();
+#ifdef GLLM_TRACE
+        if (it == 0 && lane == 0) SK_TRACE(3);
+        if (it == STAGES && lane == 0) SK_TRACE(4);
+#endif
         if (elect_one()) {
           const uint8_t* sw = smem + s * L::STAGE_BYTES;
           const uint64_t dw = smem_desc_sw128(sw);
@@ -285,6 +307,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
       const int acc = lt & 1;
       mbar_wait(&acc_full[acc], (lt >> 1) & 1);
       tc_fence_after();
+      if (et == 0) SK_TRACE(5);
       float v[NT];
       {
         const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NT);
@@ -305,6 +328,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);  // accumulator is in registers now
+      if (et == 0) SK_TRACE(8);
       bool finish = true;
       if (nkb != kbs) {
         // tile shared with other CTAs: publish, count in, the last contributor sums all
@@ -315,6 +339,7 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
           if (m < M) mine[m * W_ROWS] = v[m];
         __threadfence();
         epi_bar();
+        if (et == 0) SK_TRACE(9);
         if (et == 0) {
           const int prev = atomicAdd(&counters[t], 1);
           const bool is_last = prev == last - first;
@@ -322,25 +347,37 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
           *last_flag = is_last ? 1u : 0u;
         }
         epi_bar();
+        if (et == 0) SK_TRACE(10);
         finish = *last_flag != 0;
         if (finish) {
           __threadfence();
+          // contributors summed in order j = first..last (deterministic); the loads of a batch of
+          // U partials are all issued before the adds, so the fix-up costs one L2 round trip per
+          // batch instead of one per contributor
+          constexpr int U = NT == 16 ? 4 : 2;
           float sum[NT];
 #pragma unroll
           for (int m = 0; m < NT; ++m) sum[m] = 0.f;
-          for (int j = first; j <= last; ++j) {
-            if (j == (int)blockIdx.x) {
+          for (int j0 = first; j0 <= last; j0 += U) {
+            float x[U][NT];
 #pragma unroll
-              for (int m = 0; m < NT; ++m) sum[m] += v[m];
-            } else {
+            for (int u = 0; u < U; ++u) {
+              const int j = j0 + u;
               const float* p = partial + (size_t)(t + j) * NT * W_ROWS + f;
+              const bool ld = j <= last && j != (int)blockIdx.x;
 #pragma unroll
-              for (int m = 0; m < NT; ++m)
-                if (m < M) sum[m] += __ldcg(p + m * W_ROWS);
+              for (int m = 0; m < NT; ++m) x[u][m] = (ld && m < M) ? __ldcg(p + m * W_ROWS) : v[m];
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (j0 + u <= last) {
+#pragma unroll
+                for (int m = 0; m < NT; ++m) sum[m] += x[u][m];
+              }
           }
 #pragma unroll
           for (int m = 0; m < NT; ++m) v[m] = sum[m];
+          if (et == 0) SK_TRACE(11);
         }
       }
       if (finish) {
@@ -350,11 +387,13 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
         skinny_epilogue<NT, MODE>(st, et, t, M, N, C, ldc, bias, residual, ldr, qa, nm, rs_sm);
         epi_bar();  // staging is reused by the next tile
       }
+      if (et == 0) SK_TRACE(6);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem_base, 2 * NT < 32 ? 32 : 2 * NT);
+  if (threadIdx.x == 0) SK_TRACE(7);
 }
 
 template <int NT, int MODE>
@@ -369,8 +408,9 @@ int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, in
     if (e != cudaSuccess) return set_cuda_error(e, "skinny gemm smem attribute");
     attr = true;
   }
+  static int tag = 0;
   cudaError_t e = launch_kernel(gemm_skinny_tcgen05<NT, MODE>, dim3(grid), dim3(THREADS), smem, st, 1, mw, mx, M, N, K,
-                                per, C, ldc, bias, res, ldr, partial, counters, qa, nm);
+                                per, C, ldc, bias, res, ldr, partial, counters, qa, nm, tag++);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm_skinny_tcgen05 launch");
   return check_launch("gemm_skinny_tcgen05");
 }
@@ -445,3 +485,12 @@ int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw
 }
 
 }  // namespace gllm
+
+#ifdef GLLM_TRACE
+// debug builds only (not in include/gllm.h): copy the trace ring [64][160][12] u64 to host
+extern "C" __attribute__((visibility("default"))) int gllm_debug_trace_read(void* host, size_t bytes) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, gllm::g_trace, bytes < sizeof(gllm::g_trace) ? bytes : sizeof(gllm::g_trace)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif

@@ -381,6 +381,11 @@ int gllm_commit_tokens(const gllm_stage* stage, const gllm_batch* batch, const i
                        reinterpret_cast<cudaStream_t>(stream));
 }
 
+int gllm_gemm_workspace_reset(void* workspace, gllm_stream_t stream) {
+  if (workspace == nullptr) return set_error(GLLM_ERR_INVALID, "null GEMM workspace");
+  return gemm_ws_reset(workspace, reinterpret_cast<cudaStream_t>(stream));
+}
+
 int gllm_gemm_bf16(const void* A, int lda, const void* B, int ldb, void* C, int ldc, int M, int N, int K,
                    const void* bias, const void* residual, int ldr, int force_bn, int force_splits, void* workspace,
                    size_t workspace_bytes, gllm_stream_t stream) {

@@ -20,7 +20,7 @@ SEQ_FIELDS = 5
 # Every symbol include/gllm.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "gllm_version", "gllm_last_error", "gllm_attention_q_tile", "gllm_stage_workspace_bytes",
-    "gllm_stage_forward", "gllm_commit_tokens", "gllm_gemm_bf16", "gllm_gemm_swiglu_bf16", "gllm_gemm_qkv_rope_bf16",
+    "gllm_stage_forward", "gllm_commit_tokens", "gllm_gemm_workspace_reset", "gllm_gemm_bf16", "gllm_gemm_swiglu_bf16", "gllm_gemm_qkv_rope_bf16",
     "gllm_rmsnorm", "gllm_silu_mul",
     "gllm_prepare_batch", "gllm_embed", "gllm_rope_kv_write", "gllm_attn_mixed_paged", "gllm_attn_mixed_paged_split",
     "gllm_attn_split_workspace_bytes", "gllm_argmax",
@@ -79,6 +79,7 @@ def load() -> C.CDLL:
         "gllm_stage_workspace_bytes": (sz, [C.POINTER(Dims)]),
         "gllm_stage_forward": (i, [C.POINTER(Stage), C.POINTER(Batch), vp]),
         "gllm_commit_tokens": (i, [C.POINTER(Stage), C.POINTER(Batch), vp, vp]),
+        "gllm_gemm_workspace_reset": (i, [vp, vp]),
         "gllm_gemm_bf16": (i, [vp, i, vp, i, vp, i, i, i, i, vp, vp, i, i, i, vp, sz, vp]),
         "gllm_gemm_swiglu_bf16": (i, [vp, i, vp, i, vp, i, i, i, i, i, i, vp, sz, vp]),
         "gllm_gemm_qkv_rope_bf16": (i, [vp, i, vp, i, vp, vp, i, i, i, i, vp, vp, vp, vp, vp, i, i, i, vp, sz, vp]),
