@@ -128,7 +128,8 @@ def run_cpu_path(spec, requests, steps: int, warmup: int, sample_layers: int = 2
     from paper_2504_14775_b200.workload import prompt_token_ids
 
     model = CpuSlice(spec, sample_layers, threads=threads)
-    hist = {r.id: list(prompt_token_ids(r.id, r.input_tokens, spec.vocab)) for r in requests}
+    hist = {r.id: list(prompt_token_ids(r.id, r.input_tokens, spec.vocab, getattr(r, "token_seed", None)))
+            for r in requests}
     per_step = []
     t_start = None
     state = {"warm": warm_decodes > 0 or warm_max_iters > 0, "it": 0}

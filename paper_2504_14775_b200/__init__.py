@@ -57,8 +57,10 @@ from .workload import (
     RequestSpec,
     builtin_length_table,
     generate_arrivals,
+    load_azure_trace,
     load_trace,
     prompt_token_ids,
+    resample_arrivals,
     sample_lengths,
     save_trace,
     synthesize_requests,

@@ -184,5 +184,6 @@ class StageWorker:
 
 def default_prompt_source(specs_by_id: dict, vocab: int):
     def src(rid: int) -> np.ndarray:
-        return prompt_token_ids(rid, specs_by_id[rid].input_tokens, vocab)
+        r = specs_by_id[rid]
+        return prompt_token_ids(rid, r.input_tokens, vocab, getattr(r, "token_seed", None))
     return src

@@ -2,6 +2,7 @@
 
     python tools/sweep.py --model qwen2.5-14b --rates 4,16,64 --n-requests 300 \
         [--scheduler throttle|sarathi] [--out profiles/r1b_sweep_c3.csv]
+        [--trace-file trace.jsonl|azure.csv]   # replay a recorded trace, arrivals resampled per rate
 
 For each rate: the same ShareGPT-like trace (`workload.py:27-38`, lengths seed 1) with
 Poisson(rate, seed 0) arrivals is served end to end by `ServingEngine` (Token Throttling
@@ -19,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import csv
+import dataclasses
 import json
 import os
 import sys
@@ -35,6 +37,8 @@ def main():
     ap.add_argument("--n-requests", type=int, default=300)
     ap.add_argument("--scheduler", default="throttle", choices=["throttle", "sarathi"])
     ap.add_argument("--out", default="")
+    ap.add_argument("--trace-file", default="", help="JSONL trace or Azure-style CSV; its first --n-requests "
+                    "requests are replayed at each rate (Poisson arrivals, seed 0, as resample_rate_per_s)")
     a = ap.parse_args()
 
     import torch
@@ -44,12 +48,18 @@ def main():
     from paper_2504_14775_b200.executor import LocalExecutor
     from paper_2504_14775_b200.modelspec import MODELS
     from paper_2504_14775_b200.serving import ServingEngine
-    from paper_2504_14775_b200.workload import ArrivalProcess, builtin_length_table, synthesize_requests
+    from paper_2504_14775_b200.workload import (ArrivalProcess, builtin_length_table, load_azure_trace, load_trace,
+                                                resample_arrivals, synthesize_requests)
 
     spec = MODELS[a.model]
     rates = [float(r) for r in a.rates.split(",")]
     dist = builtin_length_table("sharegpt-like")
-    traces = {r: synthesize_requests(ArrivalProcess.poisson(r, 0), dist, a.n_requests) for r in rates}
+    if a.trace_file:
+        rec = (load_azure_trace if a.trace_file.endswith(".csv") else load_trace)(a.trace_file)[:a.n_requests]
+        rec = [dataclasses.replace(q, id=i) for i, q in enumerate(rec)]  # ids 0..n-1 in arrival order
+        traces = {r: resample_arrivals(rec, r, 0) for r in rates}
+    else:
+        traces = {r: synthesize_requests(ArrivalProcess.poisson(r, 0), dist, a.n_requests) for r in rates}
     base = traces[rates[0]]   # lengths are identical across rates (length seed = arrival seed + 1)
     page = 16
     need_pages = sum(-(-(q.input_tokens + q.output_tokens) // page) for q in base)
