@@ -16,6 +16,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -42,11 +43,12 @@ def main():
     ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, max_tokens=2048, max_emit=max(a.batch, 32), seed=0)
     eng = Engine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(pages, 16), throttle=ThrottleConfig(),
                  executor=ex)
-    decode_only, ranged = [], False
+    decode_only, ranged, wall = [], False, []
     while eng.step():
         its = eng._iters
         if its and its[-1].prefill_tokens == 0 and its[-1].decode_tokens == a.batch:
             decode_only.append(its[-1].batch_seq)
+            wall.append(time.perf_counter())
             if len(decode_only) == warm // 2 and not ranged:
                 torch.cuda.synchronize()
                 torch.cuda.nvtx.range_push("decode_timed")
@@ -65,7 +67,11 @@ def main():
         hbm = 6650.0
     floor_ms = w_bytes / (hbm * 1e9) * 1e3
     med = statistics.median(ms)
+    # host wall time per decode step through the engine (planning, packing, launches, token read-back)
+    gaps = [b - a_ for a_, b in zip(wall[warm // 2:], wall[warm // 2 + 1:])]
+    wall_ms = statistics.median(gaps) * 1e3 if gaps else None
     print(json.dumps({"model": a.model, "batch": a.batch, "ctx": a.ctx, "steps": len(ms), "ms_per_step": round(med, 3),
+                      "wall_ms_per_step": round(wall_ms, 3) if wall_ms else None,
                       "weight_floor_ms": round(floor_ms, 3), "frac_of_floor": round(floor_ms / med, 3)}))
 
 
