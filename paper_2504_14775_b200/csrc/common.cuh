@@ -126,6 +126,12 @@ GLLM_DEVICE uint32_t cluster_ctarank() {
 GLLM_DEVICE void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// non-aligned cluster barrier halves: threads of different warp roles may arrive from different code
+GLLM_DEVICE void cluster_arrive_release() { asm volatile("barrier.cluster.arrive.release;" ::: "memory"); }
+GLLM_DEVICE void cluster_wait_acquire() { asm volatile("barrier.cluster.wait.acquire;" ::: "memory"); }
+GLLM_DEVICE void st_shared_cluster_f32(uint32_t cluster_addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
+}
 // shared::cta address -> the same variable's shared::cluster address in CTA `rank` of the cluster
 GLLM_DEVICE uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   uint32_t r;

@@ -11,8 +11,13 @@
 //   * fixes up tiles shared by several CTAs without waiting: each contributor writes its fp32
 //     partial (M x 128, tiny at decode sizes), fences and bumps the tile counter; the last to
 //     arrive sums the partials in contributor order (deterministic) and runs the epilogue.
+// Cluster split-K (csize > 1, few output tiles): tile t is owned by a cluster of csize CTAs,
+// rank r streaming K-blocks [r kbs / csize, (r+1) kbs / csize). Ranks 1.. write their fp32
+// partials straight into rank 0's shared memory (DSMEM) and one cluster barrier publishes them:
+// no global partials, fence, counter or L2 round trip in the launch's tail.
 // Warp roles as in gemm.cu: warp 0 TMA producer (8-stage ring), warp 1 MMA issuer, warps 2-5
 // epilogue (TMEM -> smem transpose -> bias / residual / SwiGLU / RoPE + paged KV write).
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -37,7 +42,9 @@ struct SkSmem {
   static constexpr int STAGE_OFF = 0;
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
   static constexpr int RS_OFF = EPI_OFF + NT * ST_LD * 4;  // fused-norm row scales [NT]
-  static constexpr int BAR_OFF = RS_OFF + NT * 4;
+  static constexpr int MAX_CLUSTER = 4;
+  static constexpr int RED_OFF = RS_OFF + NT * 4;  // cluster partials [MAX_CLUSTER - 1][NT][128] fp32
+  static constexpr int BAR_OFF = RED_OFF + (MAX_CLUSTER - 1) * NT * W_ROWS * 4;
   static constexpr int TOTAL = 1024 + BAR_OFF + 256;
 };
 
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, int M,
                     int N, int K, int per, bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
                     const bf16* __restrict__ residual, int ldr, float* __restrict__ partial,
-                    int* __restrict__ counters, const QkvRopeArgs qa, const RowNorm nm, int tag) {
+                    int* __restrict__ counters, const QkvRopeArgs qa, const RowNorm nm, int csize, int tag) {
   using L = SkSmem<NT>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -213,7 +220,15 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
   pdl_trigger();
   const int kbs = K / KB;
   const int work = (N / W_ROWS) * kbs;
-  const int g_begin = blockIdx.x * per, g_end = min(g_begin + per, work);
+  int g_begin, g_end;
+  if (csize > 1) {
+    const int t = blockIdx.x / csize, r = blockIdx.x % csize;  // 1-D cluster: rank = blockIdx.x % csize
+    g_begin = t * kbs + r * kbs / csize;
+    g_end = t * kbs + (r + 1) * kbs / csize;
+  } else {
+    g_begin = blockIdx.x * per;
+    g_end = min(g_begin + per, work);
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_w);
@@ -262,6 +277,11 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
         tma_load_2d_hint(&map_x, &full[s], sw + L::W_BYTES, kc, 0, pol_x);
       }
     }
+    __syncwarp();
+    if (csize > 1) {
+      cluster_arrive_release();
+      cluster_wait_acquire();
+    }
   } else if (warp == 1) {
     constexpr uint32_t idesc = idesc_bf16_f32(W_ROWS, NT);
     int it = 0, lt = 0;
@@ -291,6 +311,11 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
         __syncwarp();
       }
       g += nkb;
+    }
+    __syncwarp();
+    if (csize > 1) {
+      cluster_arrive_release();
+      cluster_wait_acquire();
     }
   } else {
     // epilogue warps 2-5: warp q = w % 4 reads TMEM lanes [32q, 32q + 32) = W rows of the tile
@@ -330,7 +355,29 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
       if (lane == 0) mbar_arrive(&acc_empty[acc]);  // accumulator is in registers now
       if (et == 0) SK_TRACE(8);
       bool finish = true;
-      if (nkb != kbs) {
+      if (csize > 1) {
+        // cluster split-K: ranks >= 1 store their partial into rank 0's smem; the barrier
+        // (release / acquire at cluster scope) publishes it; rank 0 sums ranks in order
+        const int r = blockIdx.x % csize;
+        float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
+        if (r != 0) {
+          const uint32_t dst = mapa_shared(smem_u32(red + (size_t)(r - 1) * NT * W_ROWS + f), 0);
+#pragma unroll
+          for (int m = 0; m < NT; ++m)
+            if (m < M) st_shared_cluster_f32(dst + (uint32_t)(m * W_ROWS * 4), v[m]);
+        }
+        cluster_arrive_release();
+        cluster_wait_acquire();
+        finish = r == 0;
+        if (finish) {
+          for (int j = 1; j < csize; ++j) {
+            const float* p = red + (size_t)(j - 1) * NT * W_ROWS + f;
+#pragma unroll
+            for (int m = 0; m < NT; ++m)
+              if (m < M) v[m] += p[m * W_ROWS];
+          }
+        }
+      } else if (nkb != kbs) {
         // tile shared with other CTAs: publish, count in, the last contributor sums all
         const int first = (t * kbs) / per, last = (t * kbs + kbs - 1) / per;
         float* mine = partial + (size_t)(t + blockIdx.x) * NT * W_ROWS + f;
@@ -397,8 +444,8 @@ gemm_skinny_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_cons
 }
 
 template <int NT, int MODE>
-int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, int per, int grid, bf16* C,
-                  int ldc, const bf16* bias, const bf16* res, int ldr, float* partial, int* counters,
+int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, int per, int grid, int csize,
+                  bf16* C, int ldc, const bf16* bias, const bf16* res, int ldr, float* partial, int* counters,
                   const QkvRopeArgs& qa, const RowNorm& nm, cudaStream_t st) {
   constexpr int smem = SkSmem<NT>::TOTAL;
   static bool attr = false;
@@ -409,10 +456,78 @@ int launch_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, in
     attr = true;
   }
   static int tag = 0;
-  cudaError_t e = launch_kernel(gemm_skinny_tcgen05<NT, MODE>, dim3(grid), dim3(THREADS), smem, st, 1, mw, mx, M, N, K,
-                                per, C, ldc, bias, res, ldr, partial, counters, qa, nm, tag++);
+  cudaError_t e = launch_kernel(gemm_skinny_tcgen05<NT, MODE>, dim3(grid), dim3(THREADS), smem, st, csize, mw, mx, M,
+                                N, K, per, C, ldc, bias, res, ldr, partial, counters, qa, nm, csize, tag++);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm_skinny_tcgen05 launch");
   return check_launch("gemm_skinny_tcgen05");
+}
+
+// Co-resident clusters of c CTAs for this instantiation (GPC packing), cached per c.
+template <int NT, int MODE>
+int max_active_clusters(int c) {
+  static int cache[SkSmem<NT>::MAX_CLUSTER + 1] = {};
+  if (cache[c] == 0) {
+    cudaFuncSetAttribute(gemm_skinny_tcgen05<NT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SkSmem<NT>::TOTAL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c * device_sm_count());
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SkSmem<NT>::TOTAL;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = c;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_skinny_tcgen05<NT, MODE>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cache[c] = n > 0 ? n : -1;
+  }
+  return cache[c];
+}
+
+// Cluster size for a skinny GEMM: the largest c <= 4 whose tiles x c CTAs are all co-resident and
+// cover >= 3/5 of the SMs with >= 4 K-blocks each; 1 = stream-K (many tiles: it balances any N).
+// Measured (tools/skinny_chain.py, M = 4): 40 tiles c=3 -13% vs stream-K, 32 tiles c=4 -17%,
+// 48 tiles c=2 (65% of the SMs) -9%, 32 tiles c=2 (43%) +16%; 64 tiles c=2 even.
+// GLLM_SKINNY_CLUSTER=1 forces stream-K, =2..4 forces c where it fits (A/B runs).
+template <int NT, int MODE>
+int pick_cluster(int tiles, int kbs) {
+  static const int forced = [] {
+    const char* e = getenv("GLLM_SKINNY_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  static const bool verbose = getenv("GLLM_SKINNY_VERBOSE") != nullptr;
+  const int sms = device_sm_count();
+  int pick = 1;
+  for (int c = SkSmem<NT>::MAX_CLUSTER; c >= 2 && pick == 1; --c) {
+    if (forced && c != forced) continue;
+    if (kbs / c < 4 || tiles > max_active_clusters<NT, MODE>(c)) continue;
+    if (forced || 5 * tiles * c >= 3 * sms) pick = c;
+  }
+  if (verbose)
+    fprintf(stderr, "[gllm] skinny NT=%d mode=%d tiles=%d kbs=%d -> cluster %d (co-resident clusters c=2/3/4: %d/%d/%d)\n",
+            NT, MODE, tiles, kbs, pick, max_active_clusters<NT, MODE>(2), max_active_clusters<NT, MODE>(3),
+            max_active_clusters<NT, MODE>(4));
+  return pick;
+}
+
+template <int NT, int MODE>
+int run_skinny(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, bf16* C, int ldc,
+               const bf16* bias, const bf16* res, int ldr, float* partial, int* counters, const QkvRopeArgs& qa,
+               const RowNorm& nm, cudaStream_t st) {
+  const int sms = device_sm_count();
+  const int tiles = N / W_ROWS, kbs = K / KB, work = tiles * kbs;
+  const int csize = pick_cluster<NT, MODE>(tiles, kbs);
+  int per = (work + sms - 1) / sms;
+  if (per < 4) per = 4 < kbs ? 4 : kbs;  // >= 256 of K per CTA amortises the pipeline fill
+  const int grid = csize > 1 ? tiles * csize : (work + per - 1) / per;
+  return launch_skinny<NT, MODE>(mw, mx, M, N, K, per, grid, csize, C, ldc, bias, res, ldr, partial, counters, qa,
+                                 nm, st);
 }
 
 thread_local const void* t_clean_ws = nullptr;
@@ -452,11 +567,6 @@ int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw
   const size_t need = gemm_skinny_workspace_bytes(M, N, K);
   if (workspace == nullptr || ws_bytes < need)
     return set_error(GLLM_ERR_INVALID, "skinny gemm workspace too small (%zu < %zu)", ws_bytes, need);
-  const int sms = device_sm_count();
-  const int work = (N / W_ROWS) * (K / KB);
-  int per = (work + sms - 1) / sms;
-  if (per < 4) per = 4 < K / KB ? 4 : K / KB;  // >= 256 of K per CTA amortises the pipeline fill
-  const int grid = (work + per - 1) / per;
   if (t_clean_ws != workspace) {
     cudaError_t e = cudaMemsetAsync(workspace, 0, SKINNY_COUNTER_BYTES, st);
     if (e != cudaSuccess) return set_cuda_error(e, "skinny gemm counters");
@@ -469,13 +579,12 @@ int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw
   const QkvRopeArgs qa = qkv ? *qkv : QkvRopeArgs{};
 #define GLLM_SKINNY(NTV)                                                                                     \
   if (mode == EPI_SWIGLU)                                                                                     \
-    return launch_skinny<NTV, EPI_SWIGLU>(mw, mx, M, N, K, per, grid, C, ldc, nullptr, nullptr, 0, partial,  \
-                                          counters, qa, nm, st);                                                 \
+    return run_skinny<NTV, EPI_SWIGLU>(mw, mx, M, N, K, C, ldc, nullptr, nullptr, 0, partial, counters, qa, nm, \
+                                       st);                                                                     \
   if (mode == EPI_QKV_ROPE)                                                                                   \
-    return launch_skinny<NTV, EPI_QKV_ROPE>(mw, mx, M, N, K, per, grid, C, ldc, bias, nullptr, 0, partial,   \
-                                            counters, qa, nm, st);                                               \
-  return launch_skinny<NTV, EPI_STORE>(mw, mx, M, N, K, per, grid, C, ldc, bias, residual, ldr, partial,      \
-                                       counters, qa, nm, st);
+    return run_skinny<NTV, EPI_QKV_ROPE>(mw, mx, M, N, K, C, ldc, bias, nullptr, 0, partial, counters, qa, nm, \
+                                         st);                                                                   \
+  return run_skinny<NTV, EPI_STORE>(mw, mx, M, N, K, C, ldc, bias, residual, ldr, partial, counters, qa, nm, st);
   if (nt == 16) {
     GLLM_SKINNY(16)
   } else {
