@@ -195,6 +195,16 @@ GLLM_API int gllm_attn_mixed_paged_split(const void* qkv, const int32_t* seq_inf
                                          int n_kv_heads, int head_dim, int page_size, void* out, int n_split,
                                          void* workspace, size_t workspace_bytes, gllm_stream_t stream);
 GLLM_API size_t gllm_attn_split_workspace_bytes(int n_prefill_work, int n_split, int n_kv_heads);
+/* same, with the splits chosen as gllm_stage_forward chooses them from host copies of seq_info
+ * and work: a decode-only launch of few sequences splits each sequence's pages over a cluster of
+ * up to 4 CTAs merged through distributed shared memory (no workspace); prefill KV splits follow
+ * GLLM_ATTN_SPLIT and use the workspace (may be NULL / 0 to disable them). */
+GLLM_API int gllm_attn_mixed_paged_auto(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
+                                        int n_prefill_work, const int32_t* block_table, int max_pages_per_row,
+                                        int kv_pages, const void* k_cache, const void* v_cache, int n_heads,
+                                        int n_kv_heads, int head_dim, int page_size, void* out,
+                                        const int32_t* host_seq_info, const int32_t* host_work, void* workspace,
+                                        size_t workspace_bytes, gllm_stream_t stream);
 GLLM_API int gllm_argmax(const void* logits, int rows, int vocab, int32_t* out, gllm_stream_t stream);
 
 /* ---- measurement ---- */

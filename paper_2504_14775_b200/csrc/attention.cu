@@ -30,6 +30,7 @@
 // Cache layout [page][kv_head][slot][hd] (stage.py); pages resolved through the
 // device block table. Work list: int32 (seq index, q_start) pairs, host-packed.
 #include <float.h>
+#include <stddef.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -70,6 +71,14 @@ struct DecodeSmem {
   float merge_m[NW][8];
   float merge_l[NW][8];
 };
+// KV split over a cluster (decode-only launches): every rank's (max, sum, unnormalised O) of its
+// page range lands in rank 0's copy of this block (DSMEM), placed after DecodeSmem.
+constexpr int DEC_MAX_SPLIT = 4;
+struct DecodeRed {
+  float acc[DEC_MAX_SPLIT][8][HD];
+  float m[DEC_MAX_SPLIT][8];
+  float l[DEC_MAX_SPLIT][8];
+};
 
 
 GLLM_DEVICE void cp_async16(void* dst, const void* src) {
@@ -106,15 +115,17 @@ GLLM_DEVICE void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
 }
 
 // Decode role: one query token, the G query heads of kv head `kvh` padded to a
-// 16-row MMA tile. Each warp streams its pages (w, w+4, ...) through a 2-stage
-// cp.async.bulk ring and per 16-key page issues 16 HMMA for S = Q.K^T and 16 for
+// 16-row MMA tile. Each warp streams its pages (w, w+NW, ...) of [p_begin, p_end) through a
+// 3-stage TMA ring and per 16-key page issues 16 HMMA for S = Q.K^T and 16 for
 // O += P.V (P reused from the S accumulator registers), with the online softmax
-// on quads of lanes (one query head per quad). Warps merge through smem.
+// on quads of lanes (one query head per quad). Warps merge through smem; with a KV split
+// (csize > 1) the ranks of the cluster then merge through rank 0's DecodeRed.
 template <int G, int NW>
 __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok, int kv_len,
                                             const int* __restrict__ table, const CUtensorMap* k_map,
                                             const CUtensorMap* v_map, int n_heads, int n_kv, int kvh,
-                                            int page_size, float scale_log2, bf16* __restrict__ out) {
+                                            int page_size, float scale_log2, bf16* __restrict__ out,
+                                            int csize = 1, int crank = 0) {
   static_assert(G <= 8, "decode tile holds up to 8 query heads per kv head");
   constexpr int HALF_BYTES = 16 * 128;  // one 64-dim box of a 16-slot page (8-slot pages use half)
   DecodeSmem<NW>& sm = *reinterpret_cast<DecodeSmem<NW>*>(smem_raw);
@@ -123,7 +134,9 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   const int qc = (lane & 3) * 2;     // fragment column pair
   const int qkv_w = (n_heads + 2 * n_kv) * HD;
   const uint32_t page_bytes = (uint32_t)page_size * HD * 2;
-  const int n_pages = (kv_len + page_size - 1) / page_size;
+  const int n_pages_all = (kv_len + page_size - 1) / page_size;
+  // this rank's contiguous page range (the whole sequence without a split)
+  const int p_begin = crank * n_pages_all / csize, n_pages = (crank + 1) * n_pages_all / csize;
   const int nblk = page_size / 8;    // 8-key MMA n-blocks per page (1 or 2)
 
   if (lane == 0) {
@@ -144,7 +157,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   };
   if (lane == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) {
-      const int p = warp + s * NW;
+      const int p = p_begin + warp + s * NW;
       if (p < n_pages) issue(p, s);
     }
   }
@@ -167,7 +180,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   float m_run = -FLT_MAX, l_run = 0.f;   // row qr's state, replicated across its quad
 
   int it = 0;
-  for (int p = warp; p < n_pages; p += NW, ++it) {
+  for (int p = p_begin + warp; p < n_pages; p += NW, ++it) {
     const int s = it % DEC_STAGES;
     mbar_wait(&sm.full[warp][s], (uint32_t)((it / DEC_STAGES) & 1));
     uint8_t* kp = sm.kv[warp][s][0];
@@ -270,6 +283,8 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
     }
   }
   __syncthreads();
+  DecodeRed* red = reinterpret_cast<DecodeRed*>(smem_raw + ((sizeof(DecodeSmem<NW>) + 127) & ~size_t(127)));
+  const uint32_t red_leader = csize > 1 ? mapa_shared(smem_u32(red), 0) : 0u;
   for (int i = threadIdx.x; i < G * HD; i += NW * 32) {
     const int h = i / HD, d = i % HD;
     float mx = -FLT_MAX;
@@ -282,6 +297,32 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
       const float c = (mw == -FLT_MAX) ? 0.f : exp2f(mw - mx);
       num += sm.merge_acc[w][h][d] * c;
       den += sm.merge_l[w][h] * c;
+    }
+    if (csize == 1) {
+      out[(size_t)tok * (n_heads * HD) + (kvh * G + h) * HD + d] = f2bf(den > 0.f ? num / den : 0.f);
+    } else {
+      // this rank's (max, sum, unnormalised O) into slot crank of rank 0's DecodeRed
+      const uint32_t base = red_leader;
+      st_shared_cluster_f32(base + (uint32_t)(offsetof(DecodeRed, acc) + ((crank * 8 + h) * HD + d) * 4), num);
+      if (d == 0) {
+        st_shared_cluster_f32(base + (uint32_t)(offsetof(DecodeRed, m) + (crank * 8 + h) * 4), mx);
+        st_shared_cluster_f32(base + (uint32_t)(offsetof(DecodeRed, l) + (crank * 8 + h) * 4), den);
+      }
+    }
+  }
+  if (csize == 1) return;
+  cluster_sync();  // release / acquire at cluster scope: every rank's slot is visible to rank 0
+  if (crank != 0) return;
+  for (int i = threadIdx.x; i < G * HD; i += NW * 32) {
+    const int h = i / HD, d = i % HD;
+    float mx = -FLT_MAX;
+    for (int r = 0; r < csize; ++r) mx = fmaxf(mx, red->m[r][h]);
+    float num = 0.f, den = 0.f;
+    for (int r = 0; r < csize; ++r) {
+      const float mr = red->m[r][h];
+      const float c = (mr == -FLT_MAX) ? 0.f : exp2f(mr - mx);
+      num += red->acc[r][h][d] * c;
+      den += red->l[r][h] * c;
     }
     out[(size_t)tok * (n_heads * HD) + (kvh * G + h) * HD + d] = f2bf(den > 0.f ? num / den : 0.f);
   }
@@ -703,12 +744,14 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 2 : 1)
 attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
                    const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
                    const int* __restrict__ block_table, int mpr, int n_heads, int n_kv, int page_size,
-                   float scale_log2, bf16* __restrict__ out) {
+                   float scale_log2, bf16* __restrict__ out, int csize) {
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   pdl_trigger();
   pdl_wait();
-  const int kvh = blockIdx.x;   // kv heads fastest: a work item's CTAs launch together
+  // kv heads fastest: a work item's CTAs launch together; with a KV split the csize ranks of one
+  // (item, kv head) are consecutive in x and form one cluster
+  const int kvh = blockIdx.x / csize, crank = blockIdx.x % csize;
   const int item = blockIdx.y;
   const int sidx = work[2 * item];
   const int q0 = work[2 * item + 1];
@@ -716,7 +759,7 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_const
   const int row_id = si[0], start = si[1], tok_off = si[3];
   const int* table = block_table + (size_t)row_id * mpr;
   decode_role<G, NW>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh,
-                     page_size, scale_log2, out);
+                     page_size, scale_log2, out, csize, crank);
 }
 
 // Query tokens per prefill work item (a decode, n_new == 1, is always one item).
@@ -733,12 +776,40 @@ size_t attention_split_bytes(int n_items, int n_split, int n_kv) {
   return (size_t)n_items * n_split * n_kv * PTILES * PM * (HD + 2) * sizeof(float);
 }
 
+// Co-resident clusters of c 8-warp decode CTAs (cached per G and c).
+template <int G>
+static int decode_max_clusters(int c, size_t smem) {
+  static int cache[DEC_MAX_SPLIT + 1] = {};
+  if (cache[c] == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c * device_sm_count());
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = c;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, attn_decode_kernel<G, 8>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cache[c] = n > 0 ? n : -1;
+  }
+  return cache[c];
+}
+
 template <bool PREFILL, int G>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
                        int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
-                       float scale_log2, bf16* out, cudaStream_t st, const AttnSplit& sp = AttnSplit{}) {
+                       float scale_log2, bf16* out, cudaStream_t st, const AttnSplit& sp = AttnSplit{},
+                       int dec_pages = 0) {
   constexpr size_t smem_pf = sizeof(PrefillSmem) + 1024;
-  constexpr size_t smem4 = sizeof(DecodeSmem<4>) + 1024, smem8 = sizeof(DecodeSmem<8>) + 1024;
+  constexpr size_t smem4 = sizeof(DecodeSmem<4>) + 1024;
+  constexpr size_t smem8 = ((sizeof(DecodeSmem<8>) + 127) & ~size_t(127)) + sizeof(DecodeRed) + 1024;
   static bool attr = false;
   if (!attr) {
     const void* fns[3] = {(const void*)attn_prefill_kernel<G>, (const void*)attn_decode_kernel<G, 4>,
@@ -772,11 +843,32 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
     }
     return 0;
   } else {
-    const bool wide = (long)n_work * n_kv <= device_sm_count();  // one wave of 8-warp CTAs
-    cudaError_t e = wide ? launch_kernel(attn_decode_kernel<G, 8>, grid, dim3(256), smem8, st, 1, km, vm, qkv, seq_info,
-                                         work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out)
+    const int sms = device_sm_count();
+    const long items = (long)n_work * n_kv;
+    const bool wide = items <= sms;  // one wave of 8-warp CTAs
+    // KV split (dec_pages = the longest decode's pages, 0 = unknown / not decode-only): the
+    // fewest ranks that bring every warp to <= DEC_STAGES pages (one memory round trip), while
+    // all clusters stay co-resident in one wave
+    int csize = 1;
+    if (wide && dec_pages > DEC_STAGES * 8) {
+      static const int forced = [] {
+        const char* e = getenv("GLLM_DECODE_SPLIT");  // 1 = off, 2..4 = forced where it fits (A/B)
+        return e ? atoi(e) : 0;
+      }();
+      int want = (dec_pages + DEC_STAGES * 8 - 1) / (DEC_STAGES * 8);
+      if (forced) want = forced;
+      for (int c = want < DEC_MAX_SPLIT ? want : DEC_MAX_SPLIT; c >= 2; --c)
+        if (items * c <= sms && items <= decode_max_clusters<G>(c, smem8)) {
+          csize = c;
+          break;
+        }
+    }
+    grid.x = n_kv * csize;
+    cudaError_t e = wide ? launch_kernel(attn_decode_kernel<G, 8>, grid, dim3(256), smem8, st, csize, km, vm, qkv,
+                                         seq_info, work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out,
+                                         csize)
                          : launch_kernel(attn_decode_kernel<G, 4>, grid, dim3(128), smem4, st, 1, km, vm, qkv, seq_info,
-                                         work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out);
+                                         work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out, 1);
     if (e != cudaSuccess) return set_cuda_error(e, "attention_decode launch");
     return check_launch("attention_decode");
   }
@@ -807,14 +899,14 @@ template <int G>
 static int launch_attn_g(int n_prefill_work, const bf16* qkv, const int* seq_info, const int* work, int n_work,
                          const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache,
                          int n_heads, int n_kv, int page_size, float scale_log2, bf16* out, cudaStream_t st,
-                         const AttnSplit& sp) {
+                         const AttnSplit& sp, int dec_pages) {
   const int n_dec = n_work - n_prefill_work;
   if (n_prefill_work == 0)
     return launch_attn<false, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
-                                 n_kv, page_size, scale_log2, out, st);
+                                 n_kv, page_size, scale_log2, out, st, AttnSplit{}, dec_pages);
   if (n_dec == 0)
     return launch_attn<true, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
-                                n_kv, page_size, scale_log2, out, st, sp);
+                                n_kv, page_size, scale_log2, out, st, sp, dec_pages);
   AttnStreams* ss = nullptr;
   if (int rc = attn_streams(&ss)) return rc;
   cudaEventRecord(ss->fork, st);
@@ -882,12 +974,20 @@ int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n
       sp.part_ml = sp.part_o + (size_t)pf * n_split * n_kv * PTILES * PM * HD;
     }
   }
+  // decode-only launch: the longest decode's page count lets the decode kernel pick a KV split
+  int dec_pages = 0;
+  if (pf == 0 && host_seq_info && host_work)
+    for (int i = 0; i < n_work; ++i) {
+      const int* si = host_seq_info + 5 * host_work[2 * i];
+      const int pages = (si[1] + host_work[2 * i + 1] + 1 + page_size - 1) / page_size;
+      dec_pages = pages > dec_pages ? pages : dec_pages;
+    }
   switch (n_heads / n_kv) {
-    case 1: return launch_attn_g<1>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
-    case 2: return launch_attn_g<2>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
-    case 4: return launch_attn_g<4>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
-    case 5: return launch_attn_g<5>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
-    case 8: return launch_attn_g<8>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp);
+    case 1: return launch_attn_g<1>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
+    case 2: return launch_attn_g<2>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
+    case 4: return launch_attn_g<4>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
+    case 5: return launch_attn_g<5>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
+    case 8: return launch_attn_g<8>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
     default: return set_error(GLLM_ERR_INVALID, "unsupported GQA group %d", n_heads / n_kv);
   }
 }

@@ -448,6 +448,18 @@ int gllm_attn_mixed_paged(const void* qkv, const int32_t* seq_info, const int32_
                          (bf16*)out, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int gllm_attn_mixed_paged_auto(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
+                               int n_prefill_work, const int32_t* block_table, int max_pages_per_row, int kv_pages,
+                               const void* k_cache, const void* v_cache, int n_heads, int n_kv_heads, int head_dim,
+                               int page_size, void* out, const int32_t* host_seq_info, const int32_t* host_work,
+                               void* workspace, size_t workspace_bytes, gllm_stream_t stream) {
+  if (!host_seq_info || !host_work) return set_error(GLLM_ERR_INVALID, "host seq_info / work copies required");
+  return attention_paged((const bf16*)qkv, seq_info, work, n_work, n_prefill_work, block_table, max_pages_per_row,
+                         kv_pages, (const bf16*)k_cache, (const bf16*)v_cache, n_heads, n_kv_heads, head_dim,
+                         page_size, (bf16*)out, reinterpret_cast<cudaStream_t>(stream), /*n_split=*/0, host_seq_info,
+                         host_work, workspace, workspace_bytes);
+}
+
 int gllm_attn_mixed_paged_split(const void* qkv, const int32_t* seq_info, const int32_t* work, int n_work,
                                 int n_prefill_work, const int32_t* block_table, int max_pages_per_row, int kv_pages,
                                 const void* k_cache, const void* v_cache, int n_heads, int n_kv_heads, int head_dim,

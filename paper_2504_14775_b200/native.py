@@ -22,7 +22,7 @@ EXPORTS = (
     "gllm_version", "gllm_last_error", "gllm_attention_q_tile", "gllm_stage_workspace_bytes",
     "gllm_stage_forward", "gllm_commit_tokens", "gllm_gemm_workspace_reset", "gllm_gemm_bf16", "gllm_gemm_swiglu_bf16", "gllm_gemm_qkv_rope_bf16",
     "gllm_rmsnorm", "gllm_silu_mul",
-    "gllm_prepare_batch", "gllm_embed", "gllm_rope_kv_write", "gllm_attn_mixed_paged", "gllm_attn_mixed_paged_split",
+    "gllm_prepare_batch", "gllm_embed", "gllm_rope_kv_write", "gllm_attn_mixed_paged", "gllm_attn_mixed_paged_split", "gllm_attn_mixed_paged_auto",
     "gllm_attn_split_workspace_bytes", "gllm_argmax",
     "gllm_launch_count", "gllm_profile_begin", "gllm_profile_end",
 )
@@ -91,6 +91,8 @@ def load() -> C.CDLL:
         "gllm_attn_mixed_paged": (i, [vp, vp, vp, i, i, vp, i, i, vp, vp, i, i, i, i, vp, vp]),
         "gllm_attn_mixed_paged_split": (i, [vp, vp, vp, i, i, vp, i, i, vp, vp, i, i, i, i, vp, i, vp, C.c_size_t,
                                             vp]),
+        "gllm_attn_mixed_paged_auto": (i, [vp, vp, vp, i, i, vp, i, i, vp, vp, i, i, i, i, vp, vp, vp, vp,
+                                           C.c_size_t, vp]),
         "gllm_attn_split_workspace_bytes": (C.c_size_t, [i, i, i]),
         "gllm_argmax": (i, [vp, i, i, vp, vp]),
         "gllm_launch_count": (C.c_ulonglong, []),

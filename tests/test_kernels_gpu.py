@@ -307,19 +307,39 @@ def test_rope_kv_write(lib):
     assert torch.equal(vc[pg, :, off], v_ref.bfloat16())
 
 
-@pytest.mark.parametrize("n_heads,n_kv", [(32, 8), (64, 8), (40, 8)])
-def test_attention_decode_only_launch(lib, n_heads, n_kv):
-    """All-decode micro-batch: the decode-only instantiation (no prefill resources) must agree too."""
+DECODE_SETS = {
+    "mixed_ctx": (0, 1, 15, 16, 17, 300, 1023, 2047),
+    "two_long": (2999, 700),          # few sequences: cluster KV split of up to 4 ranks
+    "one_very_long": (8191,),
+    "short_and_long": (5, 1500, 40),  # ranks with empty page ranges
+}
+
+
+@pytest.mark.parametrize("n_heads,n_kv,ctxs,auto", [(32, 8, "mixed_ctx", False), (64, 8, "mixed_ctx", False),
+                                                    (40, 8, "mixed_ctx", False), (32, 8, "mixed_ctx", True),
+                                                    (64, 8, "two_long", True), (40, 8, "two_long", True),
+                                                    (32, 8, "one_very_long", True), (40, 8, "short_and_long", True),
+                                                    (32, 8, "two_long", False)])
+def test_attention_decode_only_launch(lib, n_heads, n_kv, ctxs, auto):
+    """All-decode micro-batch: the decode-only instantiation (no prefill resources) must agree too;
+    `auto` passes the host metadata, so few long sequences take the cluster KV split."""
     hd, ps = 128, 16
-    seqs = [(c, 1) for c in (0, 1, 15, 16, 17, 300, 1023, 2047)]
-    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, [s + 1 for s, _ in seqs], num_pages=512, seed=3)
+    seqs = [(c, 1) for c in DECODE_SETS[ctxs]]
+    ctx = [s + 1 for s, _ in seqs]
+    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, ctx, num_pages=sum(-(-c // ps) for c in ctx) + 64, seed=3)
     T = len(seqs)
     qkv = torch.randn(T, (n_heads + 2 * n_kv) * hd, device="cuda").bfloat16()
-    info = torch.tensor([[i, s, 1, i, -1] for i, (s, _) in enumerate(seqs)], dtype=torch.int32, device="cuda")
-    work = torch.tensor([[i, 0] for i in range(T)], dtype=torch.int32, device="cuda")
+    info_h = torch.tensor([[i, s, 1, i, -1] for i, (s, _) in enumerate(seqs)], dtype=torch.int32)
+    work_h = torch.tensor([[i, 0] for i in range(T)], dtype=torch.int32)
+    info, work = info_h.cuda(), work_h.cuda()
     out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
-    lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work.data_ptr(), T, 0, table.data_ptr(), mpr, kc.shape[0],
-             kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
+    if auto:
+        lib.call("gllm_attn_mixed_paged_auto", qkv.data_ptr(), info.data_ptr(), work.data_ptr(), T, 0, table.data_ptr(),
+                 mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(),
+                 info_h.data_ptr(), work_h.data_ptr(), None, 0, lib.stream_handle())
+    else:
+        lib.call("gllm_attn_mixed_paged", qkv.data_ptr(), info.data_ptr(), work.data_ptr(), T, 0, table.data_ptr(), mpr,
+                 kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(), lib.stream_handle())
     torch.cuda.synchronize()
     g = n_heads // n_kv
     for i, (s, _) in enumerate(seqs):

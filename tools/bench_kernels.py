@@ -34,7 +34,7 @@ def timeit(fn, reps=10):
     return ts[len(ts) // 2]
 
 
-def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False, split=1):
+def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False, split=1, auto=False):
     hd = 128
     ctx = [s + n for s, n in seqs]
     pages_per = [-(-c // ps) for c in ctx]
@@ -59,11 +59,17 @@ def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False, split=1)
         work += [[i, q0] for q0 in range(0, n, qt)] if n > 1 else []
         off += n
     work = work + [[i, 0] for i, (s, n) in enumerate(seqs) if n == 1]   # prefill tiles first (as the packer)
-    info = torch.tensor(info, dtype=torch.int32, device="cuda")
-    work_t = torch.tensor(work, dtype=torch.int32, device="cuda")
+    info_h = torch.tensor(info, dtype=torch.int32)
+    work_h = torch.tensor(work, dtype=torch.int32)
+    info, work_t = info_h.cuda(), work_h.cuda()
     st = native.stream_handle()
     n_pf = max(int(force_mixed), sum(1 for i, _ in work if seqs[i][1] > 1))
-    if split > 1:
+    if auto:   # splits chosen from the host metadata, as the stage forward does
+        fn = lambda: native.call("gllm_attn_mixed_paged_auto", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(),
+                                 len(work), n_pf, table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(),
+                                 n_heads, n_kv, hd, ps, out.data_ptr(), info_h.data_ptr(), work_h.data_ptr(), None, 0,
+                                 st)
+    elif split > 1:
         ws = torch.empty(native.load().gllm_attn_split_workspace_bytes(n_pf, split, n_kv), dtype=torch.uint8, device="cuda")
         fn = lambda: native.call("gllm_attn_mixed_paged_split", qkv.data_ptr(), info.data_ptr(), work_t.data_ptr(), len(work),
                                  n_pf, table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd,
@@ -134,6 +140,13 @@ if __name__ == "__main__":
         attn_case("prefill_4x512_after2000_qwen", [(2000, 512)] * 4, n_heads=40)
         attn_case("decode256_qwen", [(600, 1)] * 256, n_heads=40)
         attn_case("decode128_70b", [(4000, 1)] * 128, n_heads=64)
+        for auto in (False, True):
+            sfx = "_auto" if auto else ""
+            attn_case("decode4_ctx512_qwen" + sfx, [(512, 1)] * 4, n_heads=40, auto=auto)
+            attn_case("decode1_ctx2048_8b" + sfx, [(2048, 1)], auto=auto)
+            attn_case("decode2_ctx3000_70b" + sfx, [(3000, 1)] * 2, n_heads=64, auto=auto)
+            attn_case("decode8_ctx8000" + sfx, [(8000, 1)] * 8, auto=auto)
+            attn_case("decode16_ctx1000" + sfx, [(1000, 1)] * 16, auto=auto)
     if a.only in ("", "gemm"):
         for M in (1, 16, 64, 128, 256, 512, 1024, 2048, 2944):
             for N, K in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)):
