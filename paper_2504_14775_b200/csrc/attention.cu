@@ -155,10 +155,23 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
     tma_load_2d(v_map, &sm.full[warp][s], sm.kv[warp][s][1], 0, row0);
     tma_load_2d(v_map, &sm.full[warp][s], sm.kv[warp][s][1] + HALF_BYTES, 64, row0);
   };
+  // Pages before the last one hold keys of earlier forwards and their block-table entries are
+  // unchanged in this forward (a decode's row was assigned when it was prefilled; seq_info and
+  // work arrive by a plain host copy ahead of the forward), so they are fetched before
+  // griddepcontrol.wait, overlapping the QKV GEMM. The last page holds this token's K/V, written
+  // by that GEMM's epilogue (and may be newly appended to the table): it waits, as does Q.
+  const int p_last = n_pages_all - 1;
   if (lane == 0) {
     for (int s = 0; s < DEC_STAGES; ++s) {
       const int p = p_begin + warp + s * NW;
-      if (p < n_pages) issue(p, s);
+      if (p < n_pages && p < p_last) issue(p, s);
+    }
+  }
+  pdl_wait();
+  if (lane == 0) {
+    for (int s = 0; s < DEC_STAGES; ++s) {
+      const int p = p_begin + warp + s * NW;
+      if (p < n_pages && p == p_last) issue(p, s);
     }
   }
   // Q as A fragments (rows >= G are zero), 8 k-steps of 16 dims.
@@ -747,8 +760,7 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_const
                    float scale_log2, bf16* __restrict__ out, int csize) {
   extern __shared__ __align__(128) uint8_t smem_dyn[];
   uint8_t* smem_raw = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  pdl_trigger();
-  pdl_wait();
+  pdl_trigger();  // decode_role waits (griddepcontrol.wait) after prefetching the settled pages
   // kv heads fastest: a work item's CTAs launch together; with a KV split the csize ranks of one
   // (item, kv head) are consecutive in x and form one cluster
   const int kvh = blockIdx.x / csize, crank = blockIdx.x % csize;
