@@ -74,8 +74,20 @@ struct RowNorm {
 };
 #ifdef __CUDACC__
 __device__ __forceinline__ float row_norm_scale(const RowNorm& nm, int row) {
+  // d / 64 partials (64-128 for the served models): loads issued 16 at a time, summed in g order
+  // (the same value as a plain sequential loop, in ~5 memory round trips instead of one per group)
+  const int G = nm.d / NORM_GROUP;
+  const float* p = nm.ss_in + row;
   float s = 0.f;
-  for (int g = 0; g < nm.d / NORM_GROUP; ++g) s += nm.ss_in[(size_t)g * nm.ld + row];
+  int g = 0;
+  for (; g + 16 <= G; g += 16) {
+    float v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = p[(size_t)(g + j) * nm.ld];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s += v[j];
+  }
+  for (; g < G; ++g) s += p[(size_t)g * nm.ld];
   return rsqrtf(s / nm.d + nm.eps);
 }
 #endif

@@ -158,3 +158,32 @@ def test_pdl_bit_identical(cuda_ok):
     assert outs[0]["launches"] > 10
     assert outs[0]["tokens"] == outs[1]["tokens"]
     assert outs[0]["logits_sha256"] == outs[1]["logits_sha256"]
+
+
+@pytest.mark.parametrize("lookahead", [True, False])
+def test_wall_clock_serving_decision_replay(cuda_ok, lookahead):
+    """SURVEY §8(c)(i) on the GPU: the wall-clock serving loop (host planning overlapped with the
+    device when `lookahead`) drives real stage kernels; every logged schedule point, replayed
+    through the oracle planner on its snapshot, gives the same plan, and every request completes."""
+    from oracle.sched_ref import plan
+    from paper_2504_14775_b200.executor import LocalExecutor
+    from paper_2504_14775_b200.modelspec import MODELS
+    from paper_2504_14775_b200.serving import ServingEngine
+
+    spec = MODELS["llama3-8b"].with_layers(2)
+    reqs = [RequestSpec(i, 2.0 * i, 40 + (37 * i) % 300, 3 + (11 * i) % 17) for i in range(24)]
+    pages, ps = 1024, 16
+    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=ps, max_tokens=1024, max_emit=32, seed=5)
+    thr = ThrottleConfig(T=4, max_p=512, min_p=32)
+    eng = ServingEngine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(pages, ps), throttle=thr,
+                        executor=ex, record_decisions=True, lookahead=lookahead)
+    raw = eng.run()
+    for r in raw.requests:
+        assert r.completion_ms is not None and r.arrival_ms <= r.first_token_ms <= r.completion_ms
+        assert len(ex.outputs[r.id]) == r.output_tokens
+    assert raw.preemptions == 0
+    assert len(eng.decisions) > 0
+    for seq, (wp, rd, free, waiting, ready, pq, dq), dec, chunks in eng.decisions:
+        want = plan("throttle", wp, rd, free, pages, ps, 1, [(rid, pq[rid][0], pq[rid][1]) for rid in waiting],
+                    [(rid, dq[rid]) for rid in ready], (thr.T, thr.max_p, thr.min_p, thr.kv_thresh, "combined"), 2048)
+        assert (dec, chunks) == want[:2], seq
