@@ -595,8 +595,20 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     return e ? atoi(e) : 2;
   }();
   int bn = force_bn, cg_pick = 0;
+  bool whole_k = false;  // medium M, short K: one wave of 2-CTA BN=128 tiles, no split-K
   if (bn == 0) {
     bn = 256;
+    // 2 or 4 row tiles (M in 129-256 / 385-512) with few output tiles: when every 256-row x
+    // 128-column tile pair fits one wave and K is short, whole-K 2-CTA tiles beat split-K
+    // (no partials, no reduce launch, fused QKV epilogue kept). Measured at M = 214: QKV
+    // 7168x5120 39.9 -> 28.7 us, O 5120x5120 35.8 -> 26.7 us; at K = 27648 split-K stays ahead
+    // (87 vs 92 us: 80 CTAs cannot stream the weights alone).
+    if (m_tiles <= 4 && m_tiles % 2 == 0 && force_splits == 0 && cg_pref == 2 && N % 128 == 0 && K <= 8192 &&
+        (long)(m_tiles / 2) * (N / 128) * 2 <= num_sms) {
+      bn = 128;
+      cg_pick = 2;
+      whole_k = true;
+    }
     if (m_tiles > 4 && force_splits == 0) {
       struct Cand { int cg, bn; double eff; };
       const Cand cands[] = {{2, 256, 0.85}, {2, 128, 0.75}, {1, 256, 0.75}, {1, 128, 0.55}, {1, 64, 0.37}};
@@ -622,7 +634,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
   int splits = force_splits;
   if (splits == 0) {
     splits = 1;
-    const long tiles = (long)n_tiles * m_tiles;
+    const long tiles = whole_k ? num_sms : (long)n_tiles * m_tiles;
     // Split K only when one wave is not filled (HBM-bound weight streaming for small M). The
     // split count minimises waves(s) / s -- the time of a wave shrinks with 1/s -- plus the fp32
     // partials (written and re-read: 8 B per output per split, against the 2 B per weight the

@@ -110,12 +110,12 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--case", default="")
-    ap.add_argument("--gemm", default="", help="M,N,K single GEMM case")
+    ap.add_argument("--gemm", default="", help="M,N,K[,bn,splits] single GEMM case (bn/splits 0 = auto)")
     ap.add_argument("--swiglu", action="store_true")
     a = ap.parse_args()
     if a.gemm:
-        M, N, K = (int(x) for x in a.gemm.split(","))
-        gemm_case(M, N, K, swiglu=a.swiglu)
+        v = [int(x) for x in a.gemm.split(",")] + [0, 0]
+        gemm_case(v[0], v[1], v[2], bn=v[3], splits=v[4], swiglu=a.swiglu)
         raise SystemExit(0)
     if a.case:
         _orig = attn_case
