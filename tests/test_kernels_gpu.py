@@ -54,7 +54,8 @@ def test_gemm_tcgen05(lib, M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K", [(4, 5120, 5120), (1, 32000, 256), (16, 4096, 14336), (32, 6144, 4096), (31, 5120, 5120),
-                                   (7, 256, 768)])
+                                   (7, 256, 768), (48, 5120, 5120), (64, 4096, 14336), (33, 6144, 4096),
+                                   (100, 7168, 5120), (128, 5120, 5120), (65, 4096, 4096)])
 def test_gemm_skinny_stream_k(lib, M, N, K):
     """Decode-sized GEMMs (swap-AB stream-K: tiles shared by CTAs fixed up by the last arriver) vs
     fp32, with bias + residual, after a split-K GEMM has used the same workspace (its partials

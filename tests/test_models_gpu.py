@@ -15,20 +15,22 @@ from paper_2504_14775_b200.workload import prompt_token_ids  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def _check(name, n_stages=1, scheduler="throttle"):
+def _check(name, n_stages=1, scheduler="throttle", reqs=None, watch=None, pages=256):
     from oracle.model_ref import from_stage_workers
     from paper_2504_14775_b200.executor import LocalExecutor
     from paper_2504_14775_b200.modelspec import MODELS
 
     spec = MODELS[name].with_layers(2)
-    reqs = [RequestSpec(0, 0.0, 90, 4), RequestSpec(1, 0.2, 33, 3), RequestSpec(2, 1.0, 150, 2)]
-    ex = LocalExecutor(spec, reqs, num_pages=256, page_size=16, n_stages=n_stages, max_tokens=512,
-                       record_logits=True, seed=11)
-    Engine(reqs, scheduler=scheduler, pipeline=PipelineConfig(depth=n_stages), kv_config=KvConfig(256, 16),
+    reqs = reqs or [RequestSpec(0, 0.0, 90, 4), RequestSpec(1, 0.2, 33, 3), RequestSpec(2, 1.0, 150, 2)]
+    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, n_stages=n_stages, max_tokens=2048,
+                       max_emit=max(32, len(reqs)), record_logits=True, seed=11)
+    Engine(reqs, scheduler=scheduler, pipeline=PipelineConfig(depth=n_stages), kv_config=KvConfig(pages, 16),
            throttle=ThrottleConfig(T=2, min_p=16), token_budget=64, executor=ex).run()
     oracle = from_stage_workers(ex.stages)
     worst = 0.0
     for rid, pos, lg in ex.logits:
+        if watch is not None and rid not in watch:
+            continue
         r = reqs[rid]
         seq = np.concatenate([prompt_token_ids(rid, r.input_tokens, spec.vocab),
                               np.asarray(ex.outputs[rid], dtype=np.int32)])[:pos]
@@ -47,3 +49,12 @@ def test_model_shape_logits(cuda_ok, name):
 
 def test_two_stage_split_and_sarathi(cuda_ok):
     _check("qwen2.5-14b", n_stages=2, scheduler="sarathi")
+
+
+@pytest.mark.parametrize("name,n_req", [("llama3-8b", 40), ("qwen2.5-14b", 100)])
+def test_wide_decode_batches(cuda_ok, name, n_req):
+    """Decode steps of 33-128 sequences (128-row tiles with split-K or whole-K tiles, the split-K
+    QKV path with its separate RoPE + KV-write pass, fused-norm row scales in the split-K reduce)
+    vs the fp32 oracle."""
+    reqs = [RequestSpec(i, 0.0, 12 + (7 * i) % 29, 3) for i in range(n_req)]
+    _check(name, reqs=reqs, watch={0, 17, n_req - 1}, pages=1024)
