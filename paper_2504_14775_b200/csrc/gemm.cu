@@ -609,6 +609,14 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       cg_pick = 2;
       whole_k = true;
     }
+    // One row tile (33-128 tokens past the decode kernel), short K: whole-K tiles of the
+    // narrowest width the epilogue allows when they fill >= 1/4 of one wave (in a PDL chain at
+    // M = 100: QKV 7168x5120 27.4 -> 21.7 us, 6144x4096 24.2 -> 18.2 us; K = 14336 stays split)
+    if (m_tiles == 1 && force_splits == 0 && K <= 8192 && N % min_bn == 0 && N / min_bn <= num_sms &&
+        4 * (N / min_bn) >= num_sms) {
+      bn = min_bn;
+      whole_k = true;
+    }
     if (m_tiles > 4 && force_splits == 0) {
       struct Cand { int cg, bn; double eff; };
       const Cand cands[] = {{2, 256, 0.85}, {2, 128, 0.75}, {1, 256, 0.75}, {1, 128, 0.55}, {1, 64, 0.37}};

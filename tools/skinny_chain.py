@@ -16,7 +16,7 @@ import torch  # noqa: E402
 from paper_2504_14775_b200 import native  # noqa: E402
 
 
-def chain_ms(M, N, K, chain, reps=10):
+def chain_ms(M, N, K, chain, reps=10, bn=0, splits=0):
     lib = native.load()
     A = torch.randn(M, K, device="cuda").bfloat16()
     Ws = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(chain)]
@@ -27,7 +27,7 @@ def chain_ms(M, N, K, chain, reps=10):
     def run():
         for W in Ws:
             native.call("gllm_gemm_bf16", A.data_ptr(), K, W.data_ptr(), K, C.data_ptr(), N, M, N, K, None, None, 0,
-                        0, 0, ws.data_ptr(), ws.numel(), st)
+                        bn, splits, ws.data_ptr(), ws.numel(), st)
 
     native.call("gllm_gemm_workspace_reset", ws.data_ptr(), st)
     run()
@@ -51,10 +51,12 @@ if __name__ == "__main__":
     ap.add_argument("--n", type=int, default=5120)
     ap.add_argument("--ks", default="1280,2560,5120,10240")
     ap.add_argument("--chain", type=int, default=24)
+    ap.add_argument("--bn", type=int, default=0, help="force the 128-row tile width (0 = auto)")
+    ap.add_argument("--splits", type=int, default=0, help="force split-K (0 = auto, 1 = whole K)")
     a = ap.parse_args()
     hbm = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6554.2
     for K in (int(k) for k in a.ks.split(",")):
-        ms = chain_ms(a.m, a.n, K, a.chain)
+        ms = chain_ms(a.m, a.n, K, a.chain, bn=a.bn, splits=a.splits)
         by = 2 * a.n * K
-        print(json.dumps({"M": a.m, "N": a.n, "K": K, "us_per_gemm": round(ms * 1e3, 2),
+        print(json.dumps({"M": a.m, "N": a.n, "K": K, "bn": a.bn, "splits": a.splits, "us_per_gemm": round(ms * 1e3, 2),
                           "floor_us": round(by / hbm / 1e3, 2), "GB/s": round(by / ms / 1e6, 1)}))
