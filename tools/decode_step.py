@@ -38,8 +38,11 @@ def main():
 
     spec = MODELS[a.model]
     warm = 40
-    reqs = [RequestSpec(i, 0.0, a.ctx, warm + a.steps + 8) for i in range(a.batch)]
-    pages = a.batch * (-(-(a.ctx + warm + a.steps + 16) // 16)) + 64
+    # the first prompts finish prefill ~batch*ctx/2048 iterations before the last: their outputs
+    # must outlast that, or the batch never runs full decode-only steps
+    pf_iters = -(-a.batch * a.ctx // 2048) + 8
+    reqs = [RequestSpec(i, 0.0, a.ctx, warm + a.steps + 8 + pf_iters) for i in range(a.batch)]
+    pages = a.batch * (-(-(a.ctx + warm + a.steps + 16 + pf_iters) // 16)) + 64
     ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, max_tokens=2048, max_emit=max(a.batch, 32), seed=0)
     eng = Engine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(pages, 16), throttle=ThrottleConfig(),
                  executor=ex)
