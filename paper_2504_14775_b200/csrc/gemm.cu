@@ -611,9 +611,11 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     }
     // One row tile (33-128 tokens past the decode kernel), short K: whole-K tiles of the
     // narrowest width the epilogue allows when they fill >= 1/4 of one wave (in a PDL chain at
-    // M = 100: QKV 7168x5120 27.4 -> 21.7 us, 6144x4096 24.2 -> 18.2 us; K = 14336 stays split)
-    if (m_tiles == 1 && force_splits == 0 && K <= 8192 && N % min_bn == 0 && N / min_bn <= num_sms &&
-        4 * (N / min_bn) >= num_sms) {
+    // M = 100: QKV 7168x5120 27.4 -> 21.7 us, 6144x4096 24.2 -> 18.2 us; K = 14336 stays split).
+    // SwiGLU (gate-up, 200+ tiles of 128) too: the persistent CTAs stream their second tiles
+    // behind the first (M = 128, 27648x5120: 91.1 -> 75.8 us; M = 100, 28672x4096: 75.7 -> 65.5).
+    if (m_tiles == 1 && force_splits == 0 && K <= 8192 && N % min_bn == 0 &&
+        (N / min_bn <= num_sms || swiglu) && 4 * (N / min_bn) >= num_sms) {
       bn = min_bn;
       whole_k = true;
     }
