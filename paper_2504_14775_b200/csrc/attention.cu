@@ -3,21 +3,21 @@
 //
 // Work item = (sequence, q_start) x kv head (grid.x). The role is uniform per CTA:
 //
-//  * decode role (the item has one query token): the CTA streams the sequence's
-//    K and V pages for its kv head straight from the paged cache with
-//    cp.async.bulk (the 1-D TMA engine): one (page, kv head) block is a
-//    contiguous page_size*256 B run, so each page costs two bulk copies and no
-//    address math per element. Every warp owns a 2-stage page ring guarded by
-//    mbarriers and walks pages w, w+4, ...; the G query heads are one 16-row
-//    HMMA tile (mma.sync m16n8k16: this GEMV-shaped work is too small for a
-//    128-row tcgen05 tile), online softmax on lane quads, warps merged through
-//    shared memory. HBM-bound by design.
+//  * decode role (the item has one query token; `attn_decode_kernel<G, NW>`): NW = 4 or 8
+//    warps each walk pages w, w+NW, ... of the sequence through a 3-stage ring filled by 2-D
+//    TMA (one box per page and 64-dim half, 128B-swizzled so the ldmatrix fragment loads are
+//    conflict-free); the G query heads are one 16-row HMMA tile (mma.sync m16n8k16: this
+//    GEMV-shaped work is too small for a 128-row tcgen05 tile), online softmax on lane
+//    quads, warps merged through shared memory. HBM-bound by design. Pages before the last
+//    one are fetched before griddepcontrol.wait (they predate this forward); a decode-only
+//    launch of few long sequences splits each sequence's pages over a cluster of up to 4
+//    CTAs whose partial (max, sum, O) rank 0 merges through distributed shared memory.
 //  * prefill role (tensor cores, its own launch `attn_prefill_kernel`): a work
 //    item is 2 x 128 (token, head) query rows of one chunk (2 x 128/G tokens x
 //    the G heads sharing the kv head), attended against the cached prefix plus
 //    the chunk's own earlier tokens in 128-key blocks, FlashAttention-style and
 //    warp-specialised: warp 8 streams K/V blocks from the paged cache with 2-D
-//    TMA (one box per page and 64-dim half, 128B-swizzled) into a 4-slot ring;
+//    TMA (one box per page and 64-dim half, 128B-swizzled) into a 5-slot ring;
 //    warp 9 issues every tcgen05.mma (S = Q.K^T with Q, K from smem; O += P.V
 //    with P read straight from TMEM, V as an MN-major smem operand); warps 0-3
 //    and 4-7 run the online softmax of query tile 0 and 1, one thread per TMEM
