@@ -10,9 +10,13 @@
 //             one of two TMEM accumulators (the epilogue drains the other)
 //   warps 2-5: epilogue, tcgen05.ld 32 lanes x 32 cols -> bf16 (+bias/+residual, or fused
 //             SiLU*mul for the interleaved gate-up weight)
-// Rows past M are zero-filled by TMA on load and masked on store, so decode
-// micro-batches (M = a few tokens) reuse the same kernel; they are HBM-bound on
-// the weight stream, and split-K spreads that stream over all 148 SMs.
+// CG = 2: a cluster of two CTAs (one TPC) computes a 256 x BN tile with tcgen05.mma
+// cta_group::2, each CTA loading its 128 A rows and half of the BN weight rows.
+// Rows past M are zero-filled by TMA on load and masked on store. Tiling per call
+// (gemm_impl): M <= 32 goes to the swap-AB decode kernel (gemm_skinny.cu); short-K GEMMs
+// with few output tiles run whole-K narrow / 2-CTA tiles; other <= 4-row-tile GEMMs
+// split K (fp32 partials + a reduce with the fused epilogue) to spread the weight stream
+// over all 148 SMs; large M picks (CG, BN) by a modelled time.
 #include <stdlib.h>
 
 #include <mutex>
