@@ -31,6 +31,9 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int GEMM_THREADS = 192;
 
+// A rows per TMA box: 64 for a single 1-CTA row tile of <= 64 tokens, else the full 128
+__host__ __device__ constexpr int a_box_rows(int M, int cg) { return (cg == 1 && M <= 64) ? 64 : BM; }
+
 template <int BN, int STAGES>
 struct GemmSmem {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -268,6 +271,17 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, 2 * BN);
+  // M <= 64 (one row tile, 1-CTA): TMA loads only the first 64 A rows of each stage (a_box_rows,
+  // same rule as the host's tensor map); the other 64 rows of every stage are zeroed once here
+  // and never written again, so the A bytes each K-block moves into smem halve
+  const int a_box = a_box_rows(M, CG);
+  if (a_box < BM) {
+    for (int s = 0; s < STAGES; ++s) {
+      uint4* z = reinterpret_cast<uint4*>(smem + s * L::STAGE_BYTES + a_box * BK * 2);
+      for (int i = threadIdx.x; i < (BM - a_box) * BK * 2 / 16; i += GEMM_THREADS) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core's operand reads
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
@@ -304,7 +318,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
           uint8_t* sb = sa + L::A_BYTES;
           const int kc = (kb0 + i) * BK;
           if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES - (BM - a_box) * BK * 2);
             tma_load_2d(&map_a, &full[s], sa, kc, am);
             tma_load_2d_hint(&map_b, &full[s], sb, kc, bn, pol_w);
           } else {
@@ -685,7 +699,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
                               : ((cg_pref == 2 && m_tiles >= 2 && bn >= 128 && m_tiles % 2 == 0) ? 2 : 1);
   CUtensorMap ma, mb;
   const int a_rows = a_rows_alloc > M ? a_rows_alloc : M;
-  if (int rc = make_map(&ma, A, a_rows, K, lda, BM)) return rc;
+  if (int rc = make_map(&ma, A, a_rows, K, lda, a_box_rows(M, cg))) return rc;
   if (int rc = make_map(&mb, B, N, K, ldb, bn / cg)) return rc;
   int rc = 0;
   if (qkv && splits > 1) {
