@@ -147,6 +147,9 @@ if __name__ == "__main__":
             attn_case("decode2_ctx3000_70b" + sfx, [(3000, 1)] * 2, n_heads=64, auto=auto)
             attn_case("decode8_ctx8000" + sfx, [(8000, 1)] * 8, auto=auto)
             attn_case("decode16_ctx1000" + sfx, [(1000, 1)] * 16, auto=auto)
+        for b in (24, 32, 48, 64):
+            for c in (512, 2000):
+                attn_case(f"decode{b}_ctx{c}_qwen", [(c, 1)] * b, n_heads=40)
     if a.only in ("", "gemm"):
         for M in (1, 16, 64, 128, 256, 512, 1024, 2048, 2944):
             for N, K in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)):
