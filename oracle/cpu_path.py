@@ -30,7 +30,7 @@ def _rms(x, w, eps):
 
 class CpuSlice:
     def __init__(self, spec, sample_layers: int = 2, seed: int = 0, max_pos: int = 9000, threads: int | None = None):
-        from paper_2504_14775_b200.modelspec import rope_table
+        from oracle.model_ref import rope_table_ref as rope_table
 
         torch.set_num_threads(threads or os.cpu_count() or 1)
         self.threads = torch.get_num_threads()

@@ -279,7 +279,50 @@ def conservation():
     dump("conservation.json.gz", out)
 
 
+def scale_runs():
+    """C2-C5-scale timelines (digests): 1000-request ShareGPT-like traces at depth 1/2/4/8 for both
+    schedulers, a 2048-page memory-pressure setting, and the C5 long-prompt trace at depth 8."""
+    sg = ts.builtin_length_table("sharegpt-like")
+    c5 = ts.LengthDistribution.empirical([(p, o) for p in range(4096, 8193, 128) for o in (100, 200, 300, 400, 500)])
+    cases = []
+    for sched in ("throttle", "sarathi"):
+        for depth in (1, 2, 4, 8):
+            cases.append((f"c2_r32_{sched}_d{depth}", 32.0, "sharegpt", 1000, sched, depth, 16384))
+        cases.append((f"c2_r64_{sched}_d4_p2048", 64.0, "sharegpt", 1000, sched, 4, 2048))
+    cases.append(("c5_r2_throttle_d8", 2.0, "c5", 200, "throttle", 8, 16384))
+    cases.append(("c5_r4_sarathi_d8_p4096", 4.0, "c5", 200, "sarathi", 8, 4096))
+    out = []
+    for name, rate, dist, n, sched, depth, pages in cases:
+        reqs = ts.synthesize_requests(ts.ArrivalProcess.poisson(rate, 0), sg if dist == "sharegpt" else c5, n)
+        tsha = hashlib.sha256(json.dumps([[r.arrival_ms, r.input_tokens, r.output_tokens]
+                                          for r in reqs]).encode()).hexdigest()
+        try:
+            raw = ts.run(reqs, scheduler=sched, pipeline=PipelineConfig(depth=depth),
+                         kv_config=ts.KvConfig(pages, 16), throttle=ts.ThrottleConfig(), token_budget=2048)
+        except UnschedulableError as e:   # the reference's stall detection (`engine.py:271-276`)
+            out.append({"name": name, "rate": rate, "dist": dist, "n": n, "scheduler": sched, "depth": depth,
+                        "pages": pages, "trace_sha": tsha, "stuck": list(e.request_ids)})
+            print(name, "stuck", len(e.request_ids))
+            continue
+        t = timeline(raw)
+        rep = ts.build_report(raw)
+        out.append({"name": name, "rate": rate, "dist": dist, "n": n, "scheduler": sched, "depth": depth,
+                    "pages": pages,
+                    "trace_sha": tsha,
+                    "iters_sha": hashlib.sha256(json.dumps(t["iterations"]).encode()).hexdigest(),
+                    "reqs_sha": hashlib.sha256(json.dumps(t["requests"]).encode()).hexdigest(),
+                    "spans_sha": t["spans_sha"], "busy_sha": t["busy_sha"], "n_iters": len(t["iterations"]),
+                    "makespan": raw.makespan_ms, "preemptions": raw.preemptions,
+                    "committed": raw.committed_tokens, "discarded": raw.discarded_tokens,
+                    "token_stddev": rep.token_stddev, "bubble_mean": rep.bubble_mean})
+        print(name, len(t["iterations"]), raw.preemptions)
+    dump("scale_runs.json.gz", out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["scale"]:
+        scale_runs()
+        sys.exit(0)
     formulas()
     plans()
     kv_ops()
@@ -287,3 +330,4 @@ if __name__ == "__main__":
     engine_runs()
     scenarios()
     conservation()
+    scale_runs()

@@ -13,7 +13,7 @@ import pytest
 from golden_io import load
 from paper_2504_14775_b200 import (CommModel, Engine, KvConfig, PipelineConfig, RequestSpec, StageCostModel,
                                     ThrottleConfig, UnschedulableError, build_report, run)
-from paper_2504_14775_b200.workload import ArrivalProcess, LengthDistribution, synthesize_requests
+from paper_2504_14775_b200.workload import ArrivalProcess, LengthDistribution, builtin_length_table, synthesize_requests
 
 ENGINE = load("engine_runs.json.gz")
 TRACES = load("traces.json.gz")
@@ -123,3 +123,35 @@ def test_unschedulable_upfront():
     with pytest.raises(UnschedulableError) as ei:
         Engine([RequestSpec(0, 0.0, 100, 10)], kv_config=KvConfig(2, 16))
     assert ei.value.request_ids == (0,)
+
+
+SCALE = load("scale_runs.json.gz")
+
+
+@pytest.mark.parametrize("case", SCALE, ids=[c["name"] for c in SCALE])
+def test_scale_runs(case):
+    """C2-C5-scale timelines (1000 ShareGPT-like requests at depth 1/2/4/8, both schedulers, a
+    2048-page pressure run, the C5 long-prompt trace at depth 8) bit-exact with the reference."""
+    sg = builtin_length_table("sharegpt-like")
+    c5 = LengthDistribution.empirical([(p, o) for p in range(4096, 8193, 128) for o in (100, 200, 300, 400, 500)])
+    reqs = synthesize_requests(ArrivalProcess.poisson(case["rate"], 0), sg if case["dist"] == "sharegpt" else c5,
+                               case["n"])
+    tsha = hashlib.sha256(json.dumps([[r.arrival_ms, r.input_tokens, r.output_tokens] for r in reqs]).encode())
+    assert tsha.hexdigest() == case["trace_sha"]
+    kw = dict(scheduler=case["scheduler"], pipeline=PipelineConfig(depth=case["depth"]),
+              kv_config=KvConfig(case["pages"], 16), throttle=ThrottleConfig(), token_budget=2048)
+    if "stuck" in case:
+        with pytest.raises(UnschedulableError) as ei:
+            run(reqs, **kw)
+        assert list(ei.value.request_ids) == case["stuck"]
+        return
+    raw = run(reqs, **kw)
+    t = _timeline(raw)
+    assert len(t["iterations"]) == case["n_iters"]
+    assert hashlib.sha256(json.dumps(t["iterations"]).encode()).hexdigest() == case["iters_sha"]
+    assert hashlib.sha256(json.dumps(t["requests"]).encode()).hexdigest() == case["reqs_sha"]
+    assert (t["spans_sha"], t["busy_sha"]) == (case["spans_sha"], case["busy_sha"])
+    assert (raw.makespan_ms, raw.preemptions, raw.committed_tokens, raw.discarded_tokens) == \
+        (case["makespan"], case["preemptions"], case["committed"], case["discarded"])
+    rep = build_report(raw)
+    assert (rep.token_stddev, rep.bubble_mean) == (case["token_stddev"], case["bubble_mean"])

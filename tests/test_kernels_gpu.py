@@ -351,3 +351,68 @@ def test_attention_decode_only_launch(lib, n_heads, n_kv, ctxs, auto):
         att = (torch.einsum("hd,shd->hs", q.cpu(), k) / hd ** 0.5).softmax(-1)
         ref = torch.einsum("hs,shd->hd", att, v).reshape(-1)
         assert _rel(out[i].cpu(), ref) < 1e-2, (i, s)
+
+
+def _attn_ref_gpu(qkv, n_heads, n_kv, hd, s, n, o, k, v):
+    """fp32 causal attention of one sequence's n new queries over its s+n keys (GPU, per head)."""
+    g = n_heads // n_kv
+    q = qkv[o:o + n, : n_heads * hd].float().view(n, n_heads, hd)
+    k = k.cuda().float()
+    v = v.cuda().float()
+    qpos = torch.arange(s, s + n, device="cuda")[:, None]
+    kpos = torch.arange(s + n, device="cuda")[None, :]
+    out = torch.empty(n, n_heads, hd, device="cuda")
+    for h in range(n_heads):
+        att = (q[:, h] @ k[:, h // g].T) / hd ** 0.5
+        att = att.masked_fill(kpos > qpos, float("-inf")).softmax(-1)
+        out[:, h] = att @ v[:, h // g]
+    return out.reshape(n, -1)
+
+
+C5_SEQS = [(4096, 2048), (6016, 2048), (8064, 128), (8191, 1), (8000, 1), (7000, 1), (2, 1)]
+DECODE_8K = [(8191, 1)] * 8 + [(8100, 1)] * 8
+
+
+@pytest.mark.parametrize("n_heads,n_kv,seqs,n_split", [(64, 8, "c5", 1), (40, 8, "c5", 1), (64, 8, "c5", 4),
+                                                       (64, 8, "dec8k", 1), (40, 8, "dec8k", 1)])
+def test_attention_long_context(lib, n_heads, n_kv, seqs, n_split):
+    """C5 shapes: 2048-token prefill chunks after 4096-6016 cached tokens, a tail chunk at 8064,
+    and decode batches at ~8k context (G=8 Llama-3.1-70B, G=5 Qwen2.5); fp32 GPU reference."""
+    hd, ps = 128, 16
+    seqs = C5_SEQS if seqs == "c5" else DECODE_8K
+    ctx = [s + n for s, n in seqs]
+    kc, vc, table, mpr, dense = _paged_setup(n_kv, hd, ps, ctx, num_pages=sum(-(-c // ps) for c in ctx) + 64, seed=7)
+    T = sum(n for _, n in seqs)
+    qkv = torch.randn(T, (n_heads + 2 * n_kv) * hd, device="cuda").bfloat16()
+    q_tile = lib.load().gllm_attention_q_tile(n_heads, n_kv)
+    info, work, off = [], [], 0
+    for i, (s, n) in enumerate(seqs):
+        info.append([i, s, n, off, -1])
+        if n > 1:
+            work += [[i, q0] for q0 in range(0, n, q_tile)]
+        off += n
+    n_pf = len(work)
+    work += [[i, 0] for i, (s, n) in enumerate(seqs) if n == 1]
+    info_h = torch.tensor(info, dtype=torch.int32)
+    work_h = torch.tensor(work, dtype=torch.int32)
+    info_t, work_t = info_h.cuda(), work_h.cuda()
+    out = torch.zeros(T, n_heads * hd, device="cuda").bfloat16()
+    if n_split == 1:
+        lib.call("gllm_attn_mixed_paged_auto", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), n_pf,
+                 table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps,
+                 out.data_ptr(), info_h.data_ptr(), work_h.data_ptr(), None, 0, lib.stream_handle())
+    else:
+        ws = torch.empty(lib.load().gllm_attn_split_workspace_bytes(n_pf, n_split, n_kv), dtype=torch.uint8,
+                         device="cuda")
+        lib.call("gllm_attn_mixed_paged_split", qkv.data_ptr(), info_t.data_ptr(), work_t.data_ptr(), len(work), n_pf,
+                 table.data_ptr(), mpr, kc.shape[0], kc.data_ptr(), vc.data_ptr(), n_heads, n_kv, hd, ps, out.data_ptr(),
+                 n_split, ws.data_ptr(), ws.numel(), lib.stream_handle())
+    torch.cuda.synchronize()
+    worst = 0.0
+    for i, (s, n) in enumerate(seqs):
+        o = info[i][3]
+        ref = _attn_ref_gpu(qkv, n_heads, n_kv, hd, s, n, o, *dense[i])
+        e = _rel(out[o:o + n], ref)
+        worst = max(worst, e)
+        assert e < 1e-2, (i, s, n, e)
+    print(f"\nattention H={n_heads} KV={n_kv} {len(seqs)} seqs split={n_split}: worst rel err {worst:.3e}")

@@ -15,30 +15,59 @@ from paper_2504_14775_b200.workload import prompt_token_ids  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def _check(name, n_stages=1, scheduler="throttle", reqs=None, watch=None, pages=256):
+def _check(name, n_stages=1, scheduler="throttle", reqs=None, watch=None, pages=256, layers=2,
+           throttle=None, token_budget=64, oracle_device="cpu", max_tokens=2048):
+    """Serve `reqs` through the engine on the GPU stages, then compare every sampled step's logits
+    (teacher forcing on the GPU's own token stream) with the fp32 oracle; returns the worst
+    relative L2 error. The oracle runs each request's final sequence once (causal: every
+    position's logits at once); `oracle_device="cuda"` = the same fp32 torch code on the GPU
+    (TF32 off) for full-depth / long-prompt cases."""
     from oracle.model_ref import from_stage_workers
     from paper_2504_14775_b200.executor import LocalExecutor
     from paper_2504_14775_b200.modelspec import MODELS
 
-    spec = MODELS[name].with_layers(2)
+    spec = MODELS[name].with_layers(layers)
     reqs = reqs or [RequestSpec(0, 0.0, 90, 4), RequestSpec(1, 0.2, 33, 3), RequestSpec(2, 1.0, 150, 2)]
-    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, n_stages=n_stages, max_tokens=2048,
+    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, n_stages=n_stages, max_tokens=max_tokens,
                        max_emit=max(32, len(reqs)), record_logits=True, seed=11)
     Engine(reqs, scheduler=scheduler, pipeline=PipelineConfig(depth=n_stages), kv_config=KvConfig(pages, 16),
-           throttle=ThrottleConfig(T=2, min_p=16), token_budget=64, executor=ex).run()
-    oracle = from_stage_workers(ex.stages)
-    worst = 0.0
+           throttle=throttle or ThrottleConfig(T=2, min_p=16), token_budget=token_budget, executor=ex).run()
+    torch.backends.cuda.matmul.allow_tf32 = False
+    oracle = from_stage_workers(ex.stages, device=oracle_device)
+    by_req: dict = {}
     for rid, pos, lg in ex.logits:
-        if watch is not None and rid not in watch:
-            continue
+        if watch is None or rid in watch:
+            by_req.setdefault(rid, []).append((pos, lg))
+    worst = worst_emul = 0.0
+    for rid, items in by_req.items():
         r = reqs[rid]
         seq = np.concatenate([prompt_token_ids(rid, r.input_tokens, spec.vocab),
-                              np.asarray(ex.outputs[rid], dtype=np.int32)])[:pos]
-        want = oracle.logits(seq)[pos - 1].numpy()
-        worst = max(worst, float(np.linalg.norm(lg - want) / np.linalg.norm(want)))
+                              np.asarray(ex.outputs[rid], dtype=np.int32)])
+        last = max(pos for pos, _ in items)
+        oracle.emulate = frozenset()
+        want = oracle.logits_at(seq[:last], [pos - 1 for pos, _ in items]).cpu().numpy()
+        for (pos, lg), w in zip(items, want):
+            worst = max(worst, float(np.linalg.norm(lg - w) / np.linalg.norm(w)))
+        if layers > 2:
+            # the same math with bf16 rounding where a bf16 implementation rounds: its own drift from
+            # fp32 is the precision floor of this random-init network at this depth
+            oracle.emulate = frozenset(("in", "resid", "qkv", "p"))
+            emul = oracle.logits_at(seq[:last], [pos - 1 for pos, _ in items]).cpu().numpy()
+            for e, w in zip(emul, want):
+                worst_emul = max(worst_emul, float(np.linalg.norm(e - w) / np.linalg.norm(w)))
     for r in reqs:
         assert len(ex.outputs[r.id]) == r.output_tokens
-    assert worst < 2e-2, (name, worst)
+    # North-star bound 2e-2 (bf16 vs fp32). At depth the fp32 network itself amplifies rounding noise
+    # (tools/precision_probe.py: a 1e-3 embedding perturbation grows 14x over 32 Llama-3-8B layers), so
+    # beyond 2 layers the bound is max(2e-2, 1.5 x the bf16-emulated oracle's drift); a kernel bug
+    # (wrong page, position, head) shows up as O(1) error, far above either.
+    bound = max(2e-2, 1.5 * worst_emul)
+    print(f"\n{name} L={layers} stages={n_stages} {scheduler}: worst logits rel err {worst:.3e} "
+          f"(bf16-emulated oracle vs fp32: {worst_emul:.3e}; bound {bound:.3e}) "
+          f"over {sum(len(v) for v in by_req.values())} sampled steps")
+    assert worst < bound, (name, worst, worst_emul)
+    del ex, oracle
+    torch.cuda.empty_cache()
     return worst
 
 
@@ -58,3 +87,27 @@ def test_wide_decode_batches(cuda_ok, name, n_req):
     vs the fp32 oracle."""
     reqs = [RequestSpec(i, 0.0, 12 + (7 * i) % 29, 3) for i in range(n_req)]
     _check(name, reqs=reqs, watch={0, 17, n_req - 1}, pages=1024)
+
+
+def test_full_depth_llama3_8b(cuda_ok):
+    """All 32 layers of the Llama-3-8B shape (full-model parity on 8B)."""
+    reqs = [RequestSpec(0, 0.0, 300, 5), RequestSpec(1, 0.3, 77, 4), RequestSpec(2, 1.0, 180, 3)]
+    _check("llama3-8b", reqs=reqs, layers=32, pages=512, oracle_device="cuda")
+
+
+@pytest.mark.parametrize("name", ["qwen2.5-14b", "qwen2.5-32b", "llama3.1-70b"])
+def test_ten_layer_stage_slices(cuda_ok, name):
+    """10-layer stage slices of the C3-C5 shapes (C5's PP=8 stage is exactly 10 layers)."""
+    reqs = [RequestSpec(0, 0.0, 260, 4), RequestSpec(1, 0.2, 41, 3), RequestSpec(2, 1.0, 130, 3)]
+    _check(name, reqs=reqs, layers=10, pages=512, oracle_device="cuda")
+
+
+@pytest.mark.parametrize("name,scheduler", [("llama3.1-70b", "sarathi"), ("llama3.1-70b", "throttle"),
+                                            ("qwen2.5-32b", "sarathi")])
+def test_long_prompts_chunked(cuda_ok, name, scheduler):
+    """C5-style 4-8k prompts served in ~2048-token chunks (Sarathi budget 2048: exact 2048 chunks;
+    Token Throttling T=1: KV-headroom-scaled chunks) on a 4-layer slice, then decodes at 8k context."""
+    reqs = [RequestSpec(0, 0.0, 8000, 3), RequestSpec(1, 0.0, 4200, 3), RequestSpec(2, 5.0, 6100, 2)]
+    _check(name, scheduler=scheduler, reqs=reqs, layers=4, pages=2048,
+           throttle=ThrottleConfig(T=1, max_p=2048, min_p=32), token_budget=2048, oracle_device="cuda",
+           max_tokens=4096)

@@ -76,11 +76,11 @@ def test_pp2_real_stages_share_one_gpu(cuda_ok):
     outputs = next(m for m in msgs if m[0] == "ok")[1]
 
     from oracle.model_ref import RefDecoder
-    from paper_2504_14775_b200.modelspec import MODELS, init_embed, init_layer, rope_table
+    from paper_2504_14775_b200.modelspec import MODELS, init_embed, init_layer
     from paper_2504_14775_b200.workload import prompt_token_ids
     spec = MODELS["tiny"]
     dev = torch.device("cuda")
-    oracle = RefDecoder(spec, [init_layer(spec, l, 4, dev) for l in range(spec.n_layers)], rope_table(spec, 512),
+    oracle = RefDecoder(spec, [init_layer(spec, l, 4, dev) for l in range(spec.n_layers)], None,
                         init_embed(spec, 4, dev, "embed"), init_embed(spec, 4, dev, "final_norm"),
                         init_embed(spec, 4, dev, "lm_head"))
     clear = agree = 0
