@@ -1,24 +1,28 @@
 """Benchmark: output tokens/s of the per-iteration serving path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        # PP=N: stage s on GPU s
 
-Workload (N=1): BASELINE config 2 — Llama-3-8B-shaped random-init bf16, PP=1 on
-one B200, ShareGPT-like lengths (`workload.py:27-38`) with Poisson arrivals,
-Token Throttling T=8 / MaxP=2048 / MinP=32 / KV_thresh=0.05, page size 16.
-A "step" is one engine iteration: schedule -> KV apply -> metadata -> stage
-forward -> argmax -> commit. Before the W warm-up steps the engine is warmed
-in (untimed) until the decode population reaches steady state, so the K timed
-steps measure the saturated serving regime.
+Workload (default, N=1): BASELINE config 2 -- Llama-3-8B-shaped random-init bf16, PP=1 on one
+B200, ShareGPT-like lengths (`workload.py:27-38`) with Poisson arrivals, Token Throttling
+T=8 / MaxP=2048 / MinP=32 / KV_thresh=0.05, page size 16. `--model/--trace/--scheduler/--rate`
+select the other configs (C3 qwen2.5-14b, C4 qwen2.5-32b + sarathi, C5 llama3.1-70b + c5 trace).
+A "step" is one engine iteration: schedule -> KV apply -> metadata -> stage forward(s) -> argmax
+-> commit. Before the W warm-up steps the engine is warmed in (untimed) until the decode
+population reaches steady state, so the K timed steps measure the saturated serving regime.
+`--whole-trace` instead serves the whole trace (non-saturated rates; BASELINE's whole-run
+output tok/s, p50 TTFT / TPOT).
 
 Reported (one JSON line on rank 0):
-  value       output tokens / sum of device time of the K micro-batches
-              (CUDA events on the launch stream; metadata already in HBM)
-  e2e         same tokens / wall time of the K steps through the public API
-              (host scheduling + pinned H2D metadata + forward + D2H tokens); the
-              serving loop plans batch i+1 while batch i runs (lookahead, serving.py)
-  roofline    dominant kernel class from a profiled pass (native CUDA-event profiler)
-  cpu_baseline the oracle CPU port (oracle/cpu_path.py) on this host
-With N>1 under torchrun the stages are split across ranks (PP=N, pipeline.py).
+  value        output tokens of the K timed micro-batches / device window on rank 0's GPU
+               (CUDA events: stage-0 start of the first timed batch -> its sampled tokens of the
+               last one committed; for PP>1 the max over ranks of each stage's window)
+  e2e          the same tokens / host wall time of the K steps through the public API (host
+               scheduling + pinned H2D metadata + forward + NCCL hops + D2H tokens)
+  roofline     dominant kernel class (native CUDA-event profiler over the stages of all ranks),
+               and `classes`: every class's max(F/F_peak, B/B_peak) fraction
+  cpu_baseline the oracle CPU port (oracle/cpu_path.py) on this host (rank 0, N=1 only), plus
+               the reference scheduler's own CPU cost (oracle/sched_ref.py, 1 thread) per iteration
 """
 
 from __future__ import annotations
@@ -26,6 +30,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -35,8 +40,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+THROTTLE = "T=8 MaxP=2048 MinP=32 thr=0.05"
 
-def parse():
+
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=30)
@@ -48,14 +55,31 @@ def parse():
     p.add_argument("--scheduler", default="throttle", choices=["throttle", "sarathi"])
     p.add_argument("--trace", default="sharegpt", choices=["sharegpt", "azure", "c5"],
                    help="length distribution: ShareGPT-like (C2-C4), Azure-like, or C5 long prompts (4-8k)")
+    p.add_argument("--whole-trace", action="store_true",
+                   help="serve the whole trace; value = finished output tokens / (last completion - first arrival)")
+    p.add_argument("--layers", type=int, default=0, help="test only: truncate the model to this many layers")
     p.add_argument("--warm-decodes", type=int, default=1024, help="untimed warm-in until this many decodes run")
     p.add_argument("--warm-max-iters", type=int, default=400)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true")
+    p.add_argument("--profile-steps", type=int, default=10)
     p.add_argument("--cpu-sample-layers", type=int, default=2)
     p.add_argument("--no-lookahead", action="store_true", help="wait for each commit before planning the next batch")
     p.add_argument("--report-dir", default="", help="write report.json / requests.csv / iterations.csv of the GPU run")
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+def config_dict(args, world: int) -> dict:
+    """The workload, identical in both arms' lines (the driver compares them)."""
+    tag = {"llama3-8b": "C2", "qwen2.5-14b": "C3", "qwen2.5-32b": "C4", "llama3.1-70b": "C5",
+           "tiny": "C1"}.get(args.model, "")
+    name = {"sharegpt": "ShareGPT-like", "azure": "Azure-like", "c5": "4-8k prompts"}[args.trace]
+    return {"workload": f"{tag}: {args.model} PP={world}, {name} Poisson {args.rate:g}/s x {args.n_requests} "
+                        f"requests, {args.scheduler} {THROTTLE}" + (" (whole trace)" if args.whole_trace else ""),
+            "model": args.model + (f"[{args.layers} layers]" if args.layers else ""), "parallelism": f"pp{world}",
+            "trace": args.trace, "rate_per_s": args.rate, "n_requests": args.n_requests,
+            "scheduler": args.scheduler, "page_size": 16,
+            "l2": "inputs larger than L2 (every stage streams GBs of weights per step)"}
 
 
 def load_peaks():
@@ -66,6 +90,7 @@ def load_peaks():
         return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
                 "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
     except Exception:
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
 
 
@@ -111,6 +136,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         os.unlink(self.file.name)
+        self.proc = None
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
 
@@ -125,13 +151,50 @@ def make_trace(args):
     return synthesize_requests(ArrivalProcess.poisson(args.rate, 0), dist, args.n_requests)
 
 
-def roofline(profile: dict, peaks: dict) -> dict:
-    """Dominant kernel class by total device time; bound from its algorithmic intensity."""
+def model_spec(args):
+    from paper_2504_14775_b200.modelspec import MODELS
+    spec = MODELS[args.model]
+    return spec.with_layers(args.layers) if args.layers else spec
+
+
+# ------------------------------------------------------------------ roofline bookkeeping
+
+
+def _traffic_for(name: str, shape: dict):
+    """ncu DRAM bytes per launch for this class AT THIS SHAPE (profiles/ncu_traffic.json is keyed by
+    class + model + (N, K) with the captured M); None on any mismatch."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            table = json.load(fh)
+    except OSError:
+        return None, None
+    for key, t in table.items():
+        if key.startswith("_") or t.get("class") != name or t.get("model") != shape.get("model"):
+            continue
+        if t.get("N") != shape.get("N") or t.get("K") != shape.get("K"):
+            continue
+        m = shape.get("M")
+        if m and t.get("M") and abs(t["M"] - m) / m > 0.15:
+            continue
+        return t["dram_bytes_per_launch"], f"profiles/ncu_traffic.json[{key}] ({t['shape']})"
+    return None, None
+
+
+def roofline(profile: dict, peaks: dict, spec=None, tokens_per_step: float | None = None) -> dict:
+    """Dominant kernel class by device time; every class's max(F/F_peak, B/B_peak) fraction."""
+    fp = peaks["bf16_tflops_sustained"] * 1e12
+    bp = peaks["hbm_gbs"] * 1e9
+    classes = {}
+    for name, e in profile.items():
+        if e["total_ms"] <= 0:
+            continue
+        t_ideal = max(e["flops"] / fp, e["bytes"] / bp)
+        classes[name] = {"ms": round(e["total_ms"], 3), "launches": e["launches"],
+                         "bound": "tensor" if e["flops"] / fp >= e["bytes"] / bp else "hbm",
+                         "frac": round(t_ideal / (e["total_ms"] * 1e-3), 4)}
     name, e = max(profile.items(), key=lambda kv: kv[1]["total_ms"])
     per_launch_ms = e["total_ms"] / e["launches"]
-    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
-    intensity = e["flops"] / e["bytes"] if e["bytes"] else float("inf")
-    if e["flops"] > 0 and intensity >= ridge:
+    if e["flops"] / fp >= e["bytes"] / bp:
         achieved = e["flops"] / e["launches"] / (per_launch_ms * 1e-3) / 1e12
         peak = peaks["bf16_tflops_sustained"]
         out = {"bound": "tensor", "unit": "TFLOP/s", "algorithmic_per_launch": e["flops"] / e["launches"]}
@@ -139,63 +202,197 @@ def roofline(profile: dict, peaks: dict) -> dict:
         achieved = e["bytes"] / e["launches"] / (per_launch_ms * 1e-3) / 1e9
         peak = peaks["hbm_gbs"]
         out = {"bound": "hbm", "unit": "GB/s", "algorithmic_per_launch": e["bytes"] / e["launches"]}
-    traffic, traffic_src = None, None
-    try:  # DRAM bytes per launch of this kernel class from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            t = json.load(fh).get(name)
-        if t:
-            traffic = t["dram_bytes_per_launch"]
-            traffic_src = f"profiles/ncu_traffic.json ({t['shape']})"
-    except OSError:
-        pass
-    # both resources at once: a class mixing bandwidth- and compute-bound work (the attention call
-    # runs decode and prefill launches concurrently) is judged against bytes/HBM + FLOPs/tensor
-    t_ideal = e["bytes"] / (peaks["hbm_gbs"] * 1e9) + e["flops"] / (peaks["bf16_tflops_sustained"] * 1e12)
-    out["frac_bytes_plus_flops"] = round(t_ideal / (e["total_ms"] * 1e-3), 4)
+    shape = {}
+    if spec is not None:
+        nk = {"gemm_gate_up": (2 * spec.d_ff, spec.d_model), "gemm_down": (spec.d_model, spec.d_ff),
+              "gemm_qkv": (spec.qkv_width, spec.d_model), "gemm_o": (spec.d_model, spec.n_heads * spec.head_dim)}
+        if name in nk:
+            shape = {"model": spec.name, "N": nk[name][0], "K": nk[name][1],
+                     "M": round(tokens_per_step) if tokens_per_step else None}
+        else:
+            shape = {"model": spec.name}
+    traffic, traffic_src = _traffic_for(name, shape)
     out.update({"kernel": name, "achieved": round(achieved, 2), "peak": peak, "frac": round(achieved / peak, 4),
                 "traffic": traffic, "traffic_src": traffic_src, "launches": e["launches"],
                 "avg_launch_ms": round(per_launch_ms, 4),
-                "peak_src": peaks["src"] + (" sustained" if out["bound"] == "tensor" else "")})
+                "peak_src": peaks["src"] + (" sustained" if out["bound"] == "tensor" else ""),
+                "classes": classes})
     return out
 
 
-def run_ours(args):
+def sched_cpu_cost(args) -> dict:
+    """The reference scheduler's CPU path: oracle/sched_ref.RefEngine -- a plain
+    restatement of `tokensim.engine.run`, rescanning every request at every schedule point exactly
+    as the reference does -- over the bench trace on the virtual clock, 1 thread; next to it this
+    package's O(active) engine on the same trace. Bounded to ~10 s."""
+    from oracle.sched_ref import RefEngine
+    from paper_2504_14775_b200 import KvConfig, PipelineConfig, ThrottleConfig
+    from paper_2504_14775_b200.engine import Engine
+
+    reqs = make_trace(args)[: min(args.n_requests, 1000)]
+    rows = [(r.id, r.arrival_ms, r.input_tokens, r.output_tokens) for r in reqs]
+    depth = max(1, args.gpus)
+    ref = RefEngine(rows, args.scheduler, depth, 1 << 20, 16)
+    t0 = time.perf_counter()
+    ref.run(stop=lambda: time.perf_counter() - t0 > 10.0)
+    t_ref = time.perf_counter() - t0
+    n_ref = len(ref.iters)
+    eng = Engine(reqs, scheduler=args.scheduler, pipeline=PipelineConfig(depth=depth),
+                 kv_config=KvConfig(1 << 20, 16), throttle=ThrottleConfig())
+    t0 = time.perf_counter()
+    n_ours = 0
+    while eng.step() and time.perf_counter() - t0 < 10.0:
+        n_ours = len(eng._iters)
+    t_ours = time.perf_counter() - t0
+    try:
+        model = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")),
+                     platform.processor())
+    except OSError:
+        model = platform.processor()
+    return {"ref_us_per_iter": round(1e6 * t_ref / max(n_ref, 1), 2), "ref_iters": n_ref,
+            "ours_us_per_iter": round(1e6 * t_ours / max(n_ours, 1), 2), "ours_iters": n_ours,
+            "cores": 1, "host_cpus": os.cpu_count(), "cpu_model": model,
+            "sample": f"{len(reqs)} requests of the bench trace, depth {depth}, virtual clock, 1 thread "
+                      "(oracle/sched_ref.py = the reference engine's algorithm; ours = EngineCore)"}
+
+
+# ------------------------------------------------------------------ distributed setup
+
+
+class _Dist:
+    def __init__(self, world: int):
+        self.world = world
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.gloo = None
+        self.dev_id = 0
+
+    def init(self):
+        import torch
+        import torch.distributed as dist
+
+        local = int(os.environ.get("LOCAL_RANK", self.rank))
+        self.dev_id = local % torch.cuda.device_count()
+        torch.cuda.set_device(self.dev_id)
+        if self.world == 1:
+            return self
+        # GLLM_PP_TRANSPORT=host: activations staged through host memory over gloo (lets all ranks
+        # share one GPU for testing); default: NCCL send/recv between the ranks' GPUs.
+        self.host_transport = os.environ.get("GLLM_PP_TRANSPORT", "nccl") == "host"
+        if self.host_transport:
+            dist.init_process_group("gloo")
+            self.gloo = dist.group.WORLD
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.dev_id))
+            self.gloo = dist.new_group(backend="gloo")
+        return self
+
+    def shared_gpu_ranks(self) -> int:
+        import torch
+        return max(1, sum(1 for r in range(self.world) if r % torch.cuda.device_count() == self.dev_id))
+
+    def allreduce(self, vals, op="sum"):
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(vals, dtype=torch.float64)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX, group=self.gloo)
+        return t.tolist()
+
+    def gather(self, obj):
+        import torch.distributed as dist
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        dist.all_gather_object(out, obj, group=self.gloo)
+        return out
+
+    def bcast(self, obj):
+        import torch.distributed as dist
+        if self.world == 1:
+            return obj
+        box = [obj]
+        dist.broadcast_object_list(box, src=0, group=self.gloo)
+        return box[0]
+
+    def close(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.destroy_process_group()
+
+
+def _num_pages(args, spec, reqs, dd: _Dist, max_tokens: int) -> int:
+    """KV pool: what the trace could ever need, capped by free HBM after weights + workspace; one
+    page table is shared by all stages (`PAPER.md:254`), so every rank takes the minimum."""
+    import torch
+
+    from paper_2504_14775_b200.modelspec import stage_layers
+    page_size = 16
+    need = sum(-(-(r.input_tokens + r.output_tokens) // page_size) for r in reqs)
+    free, _ = torch.cuda.mem_get_info()
+    free //= dd.shared_gpu_ranks()
+    L = len(stage_layers(spec.n_layers, dd.world, dd.rank))
+    w_bytes = L * spec.params_per_layer * 2 + 2 * spec.vocab * spec.d_model * 2
+    page_bytes = L * spec.kv_bytes_per_token_layer * page_size
+    ws = max_tokens * (6 * spec.d_model + 3 * spec.qkv_width + 6 * spec.d_ff) * 2 + args.n_requests * spec.vocab * 2
+    fit = int((free - w_bytes - ws - (8 << 30)) // max(page_bytes, 1))
+    pages = max(1024, min(need, fit))
+    return int(dd.allreduce([-pages], op="max")[0] * -1)
+
+
+# ------------------------------------------------------------------ the GPU arm
+
+
+def run_ours(args, dd: _Dist):
     import torch
 
     from paper_2504_14775_b200 import KvConfig, PipelineConfig, ThrottleConfig, build_report, native
-    from paper_2504_14775_b200.executor import LocalExecutor
-    from paper_2504_14775_b200.modelspec import MODELS
     from paper_2504_14775_b200.serving import ServingEngine
 
-    spec = MODELS[args.model]
+    world, rank = dd.world, dd.rank
+    spec = model_spec(args)
     reqs = make_trace(args)
+    max_tokens = (2048 + args.n_requests + 255) // 256 * 256
+    num_pages = _num_pages(args, spec, reqs, dd, max_tokens)
     page_size = 16
-    max_tokens = 2048 + args.n_requests
-    max_tokens = (max_tokens + 255) // 256 * 256
-    # KV pool: what the trace could ever need, capped by free HBM after weights + workspace (8 GB slack).
-    need_pages = sum(-(-(r.input_tokens + r.output_tokens) // page_size) for r in reqs)
-    weight_bytes = spec.n_layers * spec.params_per_layer * 2 + 2 * spec.vocab * spec.d_model * 2
-    free, _ = torch.cuda.mem_get_info()
-    page_bytes = spec.n_layers * spec.kv_bytes_per_token_layer * page_size
-    ws_guess = max_tokens * (6 * spec.d_model + 3 * spec.qkv_width + 6 * spec.d_ff) * 2 + args.n_requests * spec.vocab * 2
-    fit_pages = int((free - weight_bytes - ws_guess - (8 << 30)) // page_bytes)
-    num_pages = max(1024, min(need_pages, fit_pages))
     t_init = time.time()
-    ex = LocalExecutor(spec, reqs, num_pages=num_pages, page_size=page_size, max_tokens=max_tokens,
-                       max_emit=args.n_requests, seed=0)
+    if world > 1:
+        from paper_2504_14775_b200.pipeline import (HostTransport, MetaChannel, NcclTransport, PipelineExecutor,
+                                                    make_links, worker_loop)
+        meta = MetaChannel(dd.gloo, world)
+        transport = HostTransport(dd.gloo) if dd.host_transport else NcclTransport(rank, make_links(world))
+        if rank != 0:
+            clocks = ClockSampler(dd.dev_id)
+            clocks.start()
+            launches0 = native.launch_count()
+            out = worker_loop(spec, reqs, rank=rank, world=world, meta=meta, transport=transport,
+                              num_pages=num_pages, page_size=page_size, max_tokens=max_tokens,
+                              max_emit=args.n_requests, device=f"cuda:{dd.dev_id}")
+            clk = clocks.stop()
+            return _finish_worker(args, dd, out, clk, native.launch_count() - launches0)
+        ex = PipelineExecutor(spec, reqs, world=world, meta=meta, transport=transport, num_pages=num_pages,
+                              page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests,
+                              device=f"cuda:{dd.dev_id}")
+    else:
+        from paper_2504_14775_b200.executor import LocalExecutor
+        ex = LocalExecutor(spec, reqs, num_pages=num_pages, page_size=page_size, max_tokens=max_tokens,
+                           max_emit=args.n_requests, seed=0)
     torch.cuda.synchronize()
     init_s = time.time() - t_init
-    eng = ServingEngine(reqs, scheduler=args.scheduler, pipeline=PipelineConfig(depth=1),
+    eng = ServingEngine(reqs, scheduler=args.scheduler, pipeline=PipelineConfig(depth=world),
                         kv_config=KvConfig(num_pages, page_size), throttle=ThrottleConfig(), executor=ex,
                         lookahead=not args.no_lookahead)
-
-    state = {"phase": "warm", "timed_start": None, "timed": [], "commits": 0, "stop": False,
-             "warm_iters": 0, "launch0": 0}
-    clocks = ClockSampler()
+    launches0 = native.launch_count()
+    st = {"phase": "warm", "timed": [], "stop": False, "warm_iters": 0, "launch0": 0}
+    clocks = ClockSampler(dd.dev_id)
     W, K = args.warmup, args.steps
+    if args.whole_trace:
+        st["phase"], st["timed_start"] = "whole", time.perf_counter()
+        clocks.start()
 
     def on_commit(seq, t, n_out):
-        st = state
+        if st["phase"] == "whole":
+            st["timed"].append((seq, t, n_out))
+            return
         if st["phase"] == "warm":
             st["warm_iters"] += 1
             if eng._rd >= args.warm_decodes or st["warm_iters"] >= args.warm_max_iters:
@@ -205,41 +402,42 @@ def run_ours(args):
         if st["phase"] == "warmup":
             st["count"] += 1
             if st["count"] >= W:
-                # timed region starts here: drain the device (with lookahead one batch is already
-                # queued; its commit is skipped below so only batches launched after t0 count)
-                torch.cuda.synchronize()
+                # timed region starts here. With lookahead the batches already launched are not
+                # timed: only batches launched after t0 count (their seq > the last launched one).
                 st["phase"] = "timed"
-                st["skip"] = 0 if args.no_lookahead else 1
+                st["first_seq"] = max([s for s, _ in eng.launch_log], default=seq) + 1
                 st["timed_start"] = time.perf_counter()
-                st["t_engine"] = t
                 st["launch0"] = native.launch_count()
                 torch.cuda.nvtx.range_push("bench_timed")   # ncu --nvtx --nvtx-include bench_timed/
             return
         if st["phase"] == "timed":
-            if st["skip"]:
-                st["skip"] -= 1
+            if seq < st["first_seq"]:
                 return
             st["timed"].append((seq, t, n_out))
             if len(st["timed"]) >= K:
                 # the K-th timed batch is complete (its commit waited on its event); read the clock
-                # before synchronizing, which would also wait for the next, untimed, queued batch
+                # before anything that would wait for the next, untimed, queued batch
                 st["timed_end"] = time.perf_counter()
                 st["launch1"] = native.launch_count()
-                torch.cuda.synchronize()
                 torch.cuda.nvtx.range_pop()
                 st["clocks"] = clocks.stop()
                 st["phase"] = "profile"
                 if args.no_profile:
                     st["stop"] = True
                     return
+                torch.cuda.synchronize()
                 native.profile_begin()
+                if world > 1:
+                    ex.publish_flags = 1      # workers profile the same batches (header flag)
                 st["pcount"] = 0
             return
         if st["phase"] == "profile":
             st["pcount"] += 1
-            if st["pcount"] >= max(3, min(K, 10)):
+            if st["pcount"] >= max(3, min(K, args.profile_steps)):
                 torch.cuda.synchronize()
                 st["profile"] = native.profile_end()
+                if world > 1:
+                    ex.publish_flags = 0
                 st["stop"] = True
 
     class _Stop(Exception):
@@ -247,119 +445,180 @@ def run_ours(args):
 
     def hook(seq, t, n_out):
         on_commit(seq, t, n_out)
-        if state["stop"]:
+        if st["stop"]:
             raise _Stop
 
     try:
         eng.run(on_commit=hook)
+        if args.whole_trace:
+            st["timed_end"] = time.perf_counter()
+            st["launch1"] = native.launch_count()
+            st["clocks"] = clocks.stop()
     except _Stop:
-        ex.synchronize()
-        eng._busy = ex.stage_busy_intervals()
-        eng.makespan_ms = eng.now_ms()
-    timed = state["timed"]
-    if len(timed) < K:
+        pass
+    ex.synchronize()
+    timed = st["timed"]
+    if not args.whole_trace and len(timed) < K:
         raise RuntimeError(f"trace exhausted before {K} timed steps (got {len(timed)})")
-    dev_ms = ex.batch_device_ms()
+    seqs = [s for s, _, _ in timed]
+    first, last = min(seqs), max(seqs)
+    window_ms = ex.device_window_ms(first, last)
+    busy = ex.stage_busy_ms(first, last)
+    if world > 1:
+        ex.shutdown()
     out_tokens = sum(n for _, _, n in timed)
-    device_s = sum(dev_ms[s] for s, _, _ in timed) / 1000.0
-    wall_s = state["timed_end"] - state["timed_start"]
-    tokens_per_step = [eng._iters[s].prefill_tokens + eng._iters[s].decode_tokens for s, _, _ in timed]
+    wall_s = st["timed_end"] - st["timed_start"]
     raw = eng.raw_data()
     rep = build_report(raw)
-    res = {
-        "value": out_tokens / device_s, "wall_s": wall_s, "device_s": device_s, "out_tokens": out_tokens,
-        "e2e": out_tokens / wall_s, "tokens_per_step": statistics.mean(tokens_per_step),
-        "decodes_per_step": statistics.mean(eng._iters[s].decode_tokens for s, _, _ in timed),
-        "init_s": init_s, "num_pages": num_pages, "warm_iters": state["warm_iters"],
-        "launches": state["launch1"] - state["launch0"], "clocks": state["clocks"],
-        "profile": state.get("profile"), "report": rep, "bubble": raw.bubble_fractions(),
-        "h2d_bytes_per_step": ex.h2d_bytes_total_for([s for s, _, _ in timed]) / K,
-        "d2h_bytes_per_step": 4.0 * out_tokens / K,
-    }
-    # cost-model calibration: fit the reference StageCostModel to measured stages
-    from paper_2504_14775_b200.calibration import fit_stage_cost
     its = {it.batch_seq: it for it in raw.iterations}
-    seqs = [s for s in dev_ms if s in its and s in eng._ctx_log]
-    if len(seqs) >= 3:
-        model, diag = fit_stage_cost([its[s].total_tokens for s in seqs], [eng._ctx_log[s] for s in seqs],
-                                     [dev_ms[s] for s in seqs])
-        res["calibration"] = {"c0": model.c0, "c_tok": model.c_tok, "c_ctx": model.c_ctx, **diag}
+    res = {
+        "window_ms": window_ms, "busy_ms": busy, "wall_s": wall_s, "out_tokens": out_tokens, "K": len(timed),
+        "tokens_per_step": statistics.mean(its[s].prefill_tokens + its[s].decode_tokens for s in seqs),
+        "decodes_per_step": statistics.mean(its[s].decode_tokens for s in seqs),
+        "init_s": init_s, "num_pages": num_pages, "warm_iters": st["warm_iters"],
+        "launches": st["launch1"] - st["launch0"], "clocks": st["clocks"], "profile": st.get("profile"),
+        "report": rep, "h2d_bytes_per_step": ex.h2d_bytes_total_for(seqs) / len(timed),
+        "d2h_bytes_per_step": 4.0 * out_tokens / len(timed), "spec": spec,
+        "launches_per_batch": (native.launch_count() - launches0) / max(ex.launches, 1),
+    }
+    if world == 1:
+        # cost-model calibration: fit the reference StageCostModel to measured stages
+        from paper_2504_14775_b200.calibration import fit_stage_cost
+        dev_ms = ex.batch_device_ms()
+        seqs_c = [s for s in dev_ms if s in its and s in eng._ctx_log]
+        if len(seqs_c) >= 3:
+            model, diag = fit_stage_cost([its[s].total_tokens for s in seqs_c], [eng._ctx_log[s] for s in seqs_c],
+                                         [dev_ms[s] for s in seqs_c])
+            res["calibration"] = {"c0": model.c0, "c_tok": model.c_tok, "c_ctx": model.c_ctx, **diag}
     if args.report_dir:
         from paper_2504_14775_b200.metrics import write_report
         write_report(rep, args.report_dir, extended=True)
-    return res, spec
+    # cross-rank: timed seq range -> every worker's device window / busy time / profile / clocks
+    dd.bcast((first, last))
+    per_rank = dd.gather({"window_ms": window_ms, "busy_ms": busy, "clocks": st["clocks"],
+                          "profile": st.get("profile"), "launches_per_batch": res["launches_per_batch"]})
+    res["per_rank"] = per_rank
+    return res
+
+
+def _finish_worker(args, dd: _Dist, out: dict, clk: dict, launches: int) -> None:
+    first, last = dd.bcast(None)
+    spans = out["spans"]
+    timed = [spans[s] for s in range(first, last + 1) if s in spans]
+    window = (max(b for _, b in timed) - min(a for a, _ in timed)) if timed else 0.0
+    busy = sum(b - a for a, b in timed)
+    dd.gather({"window_ms": window, "busy_ms": busy, "clocks": clk, "profile": out.get("profile"),
+               "launches_per_batch": launches / max(out["batches"], 1)})
+    return None
+
+
+def _merge_profiles(profiles) -> dict:
+    out: dict = {}
+    for p in profiles:
+        for k, v in (p or {}).items():
+            e = out.setdefault(k, {"launches": 0, "total_ms": 0.0, "flops": 0.0, "bytes": 0.0})
+            for f in e:
+                e[f] += v[f]
+    return out
+
+
+def emit_ours(args, dd: _Dist, res: dict) -> dict:
+    world = dd.world
+    per_rank = res["per_rank"]
+    W_ms = max(r["window_ms"] for r in per_rank)
+    K = res["K"]
+    rep = res["report"]
+    spec = res["spec"]
+    prof = _merge_profiles(r["profile"] for r in per_rank)
+    rl = roofline(prof, load_peaks(), spec, res["tokens_per_step"]) if prof else None
+    bubble = [round(1.0 - r["busy_ms"] / W_ms, 4) if W_ms > 0 else None for r in per_rank]
+    clocks = per_rank[0]["clocks"] if world == 1 else {
+        "sm_mhz": statistics.median([r["clocks"]["sm_mhz"] for r in per_rank if r["clocks"].get("sm_mhz")] or [0]),
+        "sm_max_mhz": per_rank[0]["clocks"].get("sm_max_mhz"),
+        "reasons": sorted({x for r in per_rank for x in r["clocks"].get("reasons", [])}),
+        "per_rank": [r["clocks"] for r in per_rank]}
+    value = res["out_tokens"] / (W_ms / 1000.0)
+    line = {
+        "metric": "output_tokens_per_s", "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
+        "steps": K, "warmup": 0 if args.whole_trace else args.warmup,
+        "ms_per_step": round(res["wall_s"] * 1000 / K, 3),
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init weights, seeded trace, PCG64 prompt tokens)",
+        "config": config_dict(args, world),
+        "e2e": {"value": round(res["out_tokens"] / res["wall_s"], 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(res["h2d_bytes_per_step"]),
+                "d2h_bytes_per_step": int(res["d2h_bytes_per_step"])},
+        "gpu_launches": int(res["launches"] if world == 1 else
+                            round(sum(r["launches_per_batch"] for r in per_rank) * K)),
+        "roofline": rl,
+        "cpu_baseline": None,
+        "clocks": clocks,
+        "run": {"kv_pages": res["num_pages"], "tokens_per_step": round(res["tokens_per_step"], 1),
+                "decodes_per_step": round(res["decodes_per_step"], 1), "device_window_ms": round(W_ms, 3),
+                "value_def": "timed output tokens / device window (max over ranks)",
+                "transport": None if world == 1 else ("host-staged gloo (test)" if dd.host_transport else "nccl p2p")},
+        "serving": {"p50_ttft_ms": rep.ttft_p50_ms, "p50_tpot_ms": rep.tpot_p50_ms,
+                    "mean_ttft_ms": rep.ttft_mean_ms, "mean_tpot_ms": rep.tpot_mean_ms,
+                    "bubble_frac_per_stage": bubble,
+                    "bubble_def": "per stage: 1 - busy / device window of the timed batches (max over ranks); "
+                                  "the reference's [0, makespan] idle fraction over the timed region",
+                    "finished": rep.finished_requests,
+                    "token_stddev_per_iter": rep.token_stddev, "token_mean_per_iter": rep.token_mean,
+                    "output_tokens_per_s_whole_run": rep.output_tokens_per_s,
+                    "note": ("whole trace served" if args.whole_trace else
+                             "latency stats over requests finished during the run (saturating arrival rate)")},
+        "profile": {k: {"launches": v["launches"], "ms": round(v["total_ms"], 3)} for k, v in prof.items()},
+        "calibration": res.get("calibration"),
+    }
+    return line
 
 
 def cpu_baseline(args, spec):
     from oracle.cpu_path import run_cpu_path
-    from paper_2504_14775_b200.workload import ArrivalProcess, builtin_length_table, synthesize_requests
     reqs = make_trace(args)
     return run_cpu_path(spec, reqs, steps=3, warmup=1, sample_layers=args.cpu_sample_layers, time_budget_s=60.0,
                         warm_decodes=args.warm_decodes, warm_max_iters=args.warm_max_iters)
 
 
-def main():
-    args = parse()
+def run_reference(args, world: int) -> dict:
+    from oracle.cpu_path import run_cpu_path
+    spec = model_spec(args)
+    reqs = make_trace(args)
+    r = run_cpu_path(spec, reqs, steps=args.steps, warmup=args.warmup, sample_layers=args.cpu_sample_layers,
+                     time_budget_s=240.0, warm_decodes=args.warm_decodes, warm_max_iters=args.warm_max_iters)
+    return {"metric": "output_tokens_per_s", "value": r["value"], "unit": "tokens/s", "n_gpus": 0,
+            "steps": r["steps"], "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (random-init weights, seeded trace, PCG64 prompt tokens)",
+            "config": config_dict(args, world),
+            "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sched_cpu": sched_cpu_cost(args)}
+
+
+def main(argv=None):
+    args = parse(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         if rank != 0:
             return 0
-        from paper_2504_14775_b200.modelspec import MODELS
-        from oracle.cpu_path import run_cpu_path
-        spec = MODELS[args.model]
-        reqs = make_trace(args)
-        r = run_cpu_path(spec, reqs, steps=args.steps, warmup=args.warmup, sample_layers=args.cpu_sample_layers,
-                         time_budget_s=240.0, warm_decodes=args.warm_decodes, warm_max_iters=args.warm_max_iters)
-        line = {"metric": "output_tokens_per_s", "value": r["value"], "unit": "tokens/s", "n_gpus": 0,
-                "steps": r["steps"], "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
-                "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"C2: {args.model} random-init, ShareGPT-like, Poisson {args.rate}/s, "
-                                       f"{args.n_requests} requests, Token Throttling T=8", "parallelism": "cpu"},
-                "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-                                 "sample": r["sample"]},
-                "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "vs_baseline": None}
-        print(json.dumps(line))
+        print(json.dumps(run_reference(args, world)))
         return 0
-    if world > 1:
-        from paper_2504_14775_b200.pipeline import bench_pipeline
-        return bench_pipeline(args)
-    res, spec = run_ours(args)
-    peaks = load_peaks()
-    rl = roofline(res["profile"], peaks) if res["profile"] else None
-    cpu = None
-    if not args.no_cpu_baseline:
-        c = cpu_baseline(args, spec)
-        cpu = {"value": c["value"], "unit": "tokens/s", "cores": c["threads"], "kind": "port", "sample": c["sample"]}
-    rep = res["report"]
-    K = args.steps
-    line = {
-        "metric": "output_tokens_per_s", "value": round(res["value"], 2), "unit": "tokens/s", "n_gpus": 1,
-        "steps": K, "warmup": args.warmup, "ms_per_step": round(res["wall_s"] * 1000 / K, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init weights, seeded ShareGPT-like trace, PCG64 prompt tokens)",
-        "config": {"workload": f"{'C2: ' if args.model == 'llama3-8b' and args.trace == 'sharegpt' else ''}"
-                               f"{args.model} PP=1 on 1xB200, {args.trace} lengths, Poisson {args.rate}/s x "
-                               f"{args.n_requests} requests, {args.scheduler} T=8 MaxP=2048 MinP=32 thr=0.05",
-                   "model": args.model, "parallelism": "pp1", "page_size": 16, "kv_pages": res["num_pages"],
-                   "tokens_per_step": round(res["tokens_per_step"], 1),
-                   "decodes_per_step": round(res["decodes_per_step"], 1),
-                   "l2": "inputs larger than L2 (16 GB of weights streamed per step)"},
-        "e2e": {"value": round(res["e2e"], 2), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(res["h2d_bytes_per_step"]), "d2h_bytes_per_step": int(res["d2h_bytes_per_step"])},
-        "gpu_launches": res["launches"],
-        "roofline": rl,
-        "cpu_baseline": cpu,
-        "clocks": res["clocks"],
-        "serving": {"p50_ttft_ms": rep.ttft_p50_ms, "p50_tpot_ms": rep.tpot_p50_ms,
-                    "bubble_frac": res["bubble"], "finished": rep.finished_requests,
-                    "token_stddev_per_iter": rep.token_stddev, "token_mean_per_iter": rep.token_mean,
-                    "note": "latency stats over requests finished during the run (overloaded arrival rate)"},
-        "profile": {k: {"launches": v["launches"], "ms": round(v["total_ms"], 3)} for k, v in (res["profile"] or {}).items()},
-        "calibration": res.get("calibration"),
-    }
+    dd = _Dist(world).init()
+    res = run_ours(args, dd)
+    if dd.rank != 0:
+        dd.close()
+        return 0
+    line = emit_ours(args, dd, res)
+    if world == 1 and not args.no_cpu_baseline:
+        c = cpu_baseline(args, res["spec"])
+        line["cpu_baseline"] = {"value": c["value"], "unit": "tokens/s", "cores": c["threads"], "kind": "port",
+                                "sample": c["sample"], "sched_cpu": sched_cpu_cost(args)}
     print(json.dumps(line))
+    dd.close()
     return 0
 
 

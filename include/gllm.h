@@ -50,6 +50,13 @@ enum {
  *   emit     index in the sampled-token output, or -1 (no token sampled) */
 #define GLLM_SEQ_FIELDS 5
 
+/* Metadata bounds-check bits (gllm_meta_errors): ids outside the stage's tables are never
+ * written through -- deltas / prompt rows are skipped, tokens get slot -1 (no KV write). */
+#define GLLM_META_BAD_DELTA 1u  /* block-table delta row / page index / page id out of range */
+#define GLLM_META_BAD_PROMPT 2u /* prompt header row / length out of range */
+#define GLLM_META_BAD_SEQ 4u    /* seq_info row out of range or start + n_new > max_seq_len */
+#define GLLM_META_BAD_PAGE 8u   /* block-table entry of a token's position is not a valid page */
+
 /* Model/stage dimensions (Llama / Qwen2 decoder, head_dim 128). */
 typedef struct gllm_dims {
   int n_layers;     /* layers held by this stage */
@@ -175,6 +182,11 @@ GLLM_API int gllm_gemm_qkv_rope_bf16(const void* A, int lda, const void* W, int 
 GLLM_API int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* weight, void* out, int rows, int d,
                  float eps, gllm_stream_t stream);
 GLLM_API int gllm_silu_mul(const void* gate_up, int d_ff, void* out, int rows, gllm_stream_t stream);
+/* OR of GLLM_META_* bits raised by any micro-batch since the last reset (a host-mapped word the
+ * kernels write only on a violation: reading it needs no sync). `reset` != 0 clears it.
+ * The host runtime checks it after every retired micro-batch. */
+GLLM_API uint32_t gllm_meta_errors(int reset);
+
 GLLM_API int gllm_prepare_batch(const gllm_stage* stage, const gllm_batch* batch, int32_t* tok_pos, int32_t* tok_slot,
                        int32_t* tok_id, int32_t* emit_rows, gllm_stream_t stream);
 GLLM_API int gllm_embed(const int32_t* tok_id, int n_tokens, const void* embed, int d, void* out, gllm_stream_t stream);

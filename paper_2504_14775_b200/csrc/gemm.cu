@@ -110,6 +110,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
         if (gh < qa.n_heads) {
           dst = C + (size_t)row * ldc + gh * 128;
         } else {
+          if (slot < 0) continue;   // metadata failed the bounds check in expand_tokens: no KV write
           const int kvh = gh < qa.n_heads + qa.n_kv ? gh - qa.n_heads : gh - qa.n_heads - qa.n_kv;
           bf16* cache = gh < qa.n_heads + qa.n_kv ? qa.k_cache : qa.v_cache;
           dst = cache + (((size_t)page * qa.n_kv + kvh) * qa.page_size + off) * 128;

@@ -185,6 +185,7 @@ __device__ __forceinline__ void skinny_epilogue(const float* st, int et, int t, 
       if (gh < qa.n_heads) {
         dst = C + (size_t)m * ldc + gh * 128;
       } else {
+        if (slot < 0) continue;     // metadata failed the bounds check in expand_tokens: no KV write
         const int kvh = gh < qa.n_heads + qa.n_kv ? gh - qa.n_heads : gh - qa.n_heads - qa.n_kv;
         bf16* cache = gh < qa.n_heads + qa.n_kv ? qa.k_cache : qa.v_cache;
         dst = cache + (((size_t)page * qa.n_kv + kvh) * qa.page_size + off) * 128;

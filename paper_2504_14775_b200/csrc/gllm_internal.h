@@ -132,11 +132,14 @@ int silu_mul(const bf16* gu, int d_ff, bf16* out, int rows, cudaStream_t st);
 int rope_kv_write(bf16* qkv, int n_tokens, int n_heads, int n_kv, int head_dim, const int* tok_pos,
                   const int* tok_slot, const float* rope, bf16* k_cache, bf16* v_cache, int page_size,
                   cudaStream_t st);
+// bounds-checked (see kernels.cu): invalid ids are skipped / get slot -1 and set GLLM_META_* bits
 int apply_batch_metadata(const int* meta, int n_deltas, int n_prompt_rows, int* block_table, int max_pages_per_row,
-                         int* token_hist, int max_seq_len, cudaStream_t st);
+                         int* token_hist, int max_seq_len, int max_rows, int num_pages, cudaStream_t st);
 int expand_tokens(const int* seq_info, int n_seqs, const int* block_table, int max_pages_per_row,
                   const int* token_hist, int max_seq_len, int page_size, int* tok_pos, int* tok_slot, int* tok_id,
-                  int* emit_rows, const bf16* embed, int d, bf16* x_out, cudaStream_t st);
+                  int* emit_rows, const bf16* embed, int d, bf16* x_out, int max_rows, int num_pages,
+                  cudaStream_t st);
+unsigned meta_errors(int reset);
 int embed_tokens(const int* tok_id, int n_tokens, const bf16* embed, int d, bf16* out, cudaStream_t st);
 int argmax_rows(const bf16* logits, int rows, int vocab, int* out, cudaStream_t st);
 int commit_tokens(const int* seq_info, int n_seqs, const int* sampled, int* token_hist, int max_seq_len,

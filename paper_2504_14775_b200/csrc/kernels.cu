@@ -17,33 +17,77 @@
 namespace gllm {
 
 // ----------------------------------------------------------- metadata
+// Bounds checks: the host is trusted for shapes but not for ids -- a row, page index, page id
+// or position outside the stage's tables would silently corrupt another request's KV. Invalid
+// entries are skipped (block-table deltas, prompt rows) or given slot -1 (tokens; the KV-writing
+// epilogues skip those), and a bit is OR-ed into a host-mapped error word that the executor
+// reads after every micro-batch (gllm_meta_errors) -- no extra sync or copy on the fast path.
+static unsigned* g_err_host = nullptr;
+static unsigned* g_err_dev = nullptr;
+
+static unsigned* err_word() {
+  if (g_err_dev == nullptr) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&g_err_host), sizeof(unsigned), cudaHostAllocMapped) != cudaSuccess)
+      return nullptr;
+    *g_err_host = 0;
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&g_err_dev), g_err_host, 0) != cudaSuccess) {
+      g_err_dev = nullptr;
+      return nullptr;
+    }
+  }
+  return g_err_dev;
+}
+
+unsigned meta_errors(int reset) {
+  if (g_err_host == nullptr) return 0;
+  const unsigned v = *reinterpret_cast<volatile unsigned*>(g_err_host);
+  if (reset) *reinterpret_cast<volatile unsigned*>(g_err_host) = 0;
+  return v;
+}
+
+__device__ __forceinline__ void flag_error(unsigned* err, unsigned bit) {
+  if (err != nullptr) atomicOr_system(err, bit);
+#ifdef GLLM_DEBUG
+  __trap();
+#endif
+}
+
 // meta layout: deltas [n_deltas][3] = (row, page_index, page_id), then
 // prompt headers [n_prompt_rows][3] = (row, length, offset into the token area),
 // then the token area.
 __global__ void apply_metadata_kernel(const int* __restrict__ meta, int n_deltas, int n_prompt_rows,
                                       int* __restrict__ block_table, int mpr, int* __restrict__ token_hist,
-                                      int max_seq_len) {
+                                      int max_seq_len, int max_rows, int num_pages, unsigned* err) {
   const int* hdr = meta + 3 * n_deltas;
   const int* toks = hdr + 3 * n_prompt_rows;
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < n_deltas; i += blockDim.x) {
       const int row = meta[3 * i], idx = meta[3 * i + 1], page = meta[3 * i + 2];
+      if ((unsigned)row >= (unsigned)max_rows || (unsigned)idx >= (unsigned)mpr ||
+          (unsigned)page >= (unsigned)num_pages) {
+        flag_error(err, GLLM_META_BAD_DELTA);
+        continue;
+      }
       block_table[(size_t)row * mpr + idx] = page;
     }
   }
   for (int p = blockIdx.x; p < n_prompt_rows; p += gridDim.x) {
     const int row = hdr[3 * p], len = hdr[3 * p + 1], off = hdr[3 * p + 2];
+    if ((unsigned)row >= (unsigned)max_rows || len < 0 || len > max_seq_len || off < 0) {
+      if (threadIdx.x == 0) flag_error(err, GLLM_META_BAD_PROMPT);
+      continue;
+    }
     int* dst = token_hist + (size_t)row * max_seq_len;
     for (int t = threadIdx.x; t < len; t += blockDim.x) dst[t] = toks[off + t];
   }
 }
 
 int apply_batch_metadata(const int* meta, int n_deltas, int n_prompt_rows, int* block_table, int mpr,
-                         int* token_hist, int max_seq_len, cudaStream_t st) {
+                         int* token_hist, int max_seq_len, int max_rows, int num_pages, cudaStream_t st) {
   if (n_deltas == 0 && n_prompt_rows == 0) return 0;
   int blocks = n_prompt_rows > 0 ? (n_prompt_rows < 1024 ? n_prompt_rows : 1024) : 1;
   apply_metadata_kernel<<<blocks, 256, 0, st>>>(meta, n_deltas, n_prompt_rows, block_table, mpr, token_hist,
-                                                  max_seq_len);
+                                                  max_seq_len, max_rows, num_pages, err_word());
   return check_launch("apply_metadata");
 }
 
@@ -52,19 +96,28 @@ int apply_batch_metadata(const int* meta, int n_deltas, int n_prompt_rows, int* 
 __global__ void expand_tokens_kernel(const int* __restrict__ seq_info, int n_seqs, const int* __restrict__ block_table,
                                      int mpr, const int* __restrict__ token_hist, int max_seq_len, int page_size,
                                      int* __restrict__ tok_pos, int* __restrict__ tok_slot, int* __restrict__ tok_id,
-                                     int* __restrict__ emit_rows) {
+                                     int* __restrict__ emit_rows, int max_rows, int num_pages, unsigned* err) {
   const int s = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (s >= n_seqs) return;
   const int* si = seq_info + 5 * s;
   const int row = si[0], start = si[1], n = si[2], off = si[3], emit = si[4];
-  const int* table = block_table + (size_t)row * mpr;
-  const int* hist = token_hist != nullptr ? token_hist + (size_t)row * max_seq_len : nullptr;
+  const bool row_ok = (unsigned)row < (unsigned)max_rows && start >= 0 && n >= 0 && start + n <= max_seq_len &&
+                      start + n <= mpr * page_size;
+  if (!row_ok && lane == 0) flag_error(err, GLLM_META_BAD_SEQ);
+  const int* table = block_table + (size_t)(row_ok ? row : 0) * mpr;
+  const int* hist = token_hist != nullptr ? token_hist + (size_t)(row_ok ? row : 0) * max_seq_len : nullptr;
   for (int t = lane; t < n; t += 32) {
     const int pos = start + t;
-    tok_pos[off + t] = pos;
-    tok_slot[off + t] = table[pos / page_size] * page_size + pos % page_size;
-    if (tok_id != nullptr) tok_id[off + t] = hist[pos];
+    tok_pos[off + t] = row_ok ? pos : 0;
+    int slot = -1;
+    if (row_ok) {
+      const int page = table[pos / page_size];
+      if ((unsigned)page < (unsigned)num_pages) slot = page * page_size + pos % page_size;
+      else flag_error(err, GLLM_META_BAD_PAGE);
+    }
+    tok_slot[off + t] = slot;
+    if (tok_id != nullptr) tok_id[off + t] = row_ok ? hist[pos] : 0;
   }
   if (lane == 0 && emit >= 0 && emit_rows != nullptr) emit_rows[emit] = off + n - 1;
 }
@@ -80,11 +133,12 @@ __global__ void embed_kernel(const int* __restrict__ tok_id, const bf16* __restr
 
 int expand_tokens(const int* seq_info, int n_seqs, const int* block_table, int mpr, const int* token_hist,
                   int max_seq_len, int page_size, int* tok_pos, int* tok_slot, int* tok_id, int* emit_rows,
-                  const bf16* embed, int d, bf16* x_out, cudaStream_t st) {
+                  const bf16* embed, int d, bf16* x_out, int max_rows, int num_pages, cudaStream_t st) {
   if (n_seqs <= 0) return 0;
   const int warps = 8;
   expand_tokens_kernel<<<(n_seqs + warps - 1) / warps, warps * 32, 0, st>>>(
-      seq_info, n_seqs, block_table, mpr, token_hist, max_seq_len, page_size, tok_pos, tok_slot, tok_id, emit_rows);
+      seq_info, n_seqs, block_table, mpr, token_hist, max_seq_len, page_size, tok_pos, tok_slot, tok_id, emit_rows,
+      max_rows, num_pages, err_word());
   if (int rc = check_launch("expand_tokens")) return rc;
   return 0;
 }
@@ -263,14 +317,16 @@ __global__ void rope_kv_kernel(bf16* __restrict__ qkv, int n_heads, int n_kv, in
       base[j] = y1;
       base[j + half] = y2;
     } else {
+      base[j] = y1;
+      base[j + half] = y2;
+      if (slot < 0) continue;       // metadata failed the bounds check in expand_tokens
       const int kh = h - n_heads;
       bf16* dst = k_cache + (((size_t)page * n_kv + kh) * page_size + off) * hd;
       dst[j] = y1;
       dst[j + half] = y2;
-      base[j] = y1;
-      base[j + half] = y2;
     }
   }
+  if (slot < 0) return;
   // v heads: straight copy, 16 bytes per thread
   const int vvec = n_kv * hd / 8;
   const uint4* vsrc = reinterpret_cast<const uint4*>(row + (n_heads + n_kv) * hd);

@@ -202,11 +202,11 @@ static int prepare(const gllm_stage& S, const gllm_batch& B, int* tok_pos, int* 
   const gllm_dims& d = S.dims;
   MetaView mv = meta_view(B);
   if (int rc = apply_batch_metadata(mv.deltas, B.n_deltas, S.token_hist ? B.n_prompts : 0, S.block_table,
-                                    d.max_pages_per_row, S.token_hist, d.max_seq_len, st))
+                                    d.max_pages_per_row, S.token_hist, d.max_seq_len, d.max_rows, d.num_pages, st))
     return rc;
   return expand_tokens(mv.seq_info, B.n_seqs, S.block_table, d.max_pages_per_row, S.is_first ? S.token_hist : nullptr,
                        d.max_seq_len, d.page_size, tok_pos, tok_slot, S.is_first ? tok_id : nullptr,
-                       S.is_last ? emit_rows : nullptr, nullptr, d.d_model, nullptr, st);
+                       S.is_last ? emit_rows : nullptr, nullptr, d.d_model, nullptr, d.max_rows, d.num_pages, st);
 }
 
 static int validate(const gllm_stage* S, const gllm_batch* B) {
@@ -419,6 +419,8 @@ int gllm_rmsnorm(const void* x, int ldx, const int32_t* row_index, const void* w
 int gllm_silu_mul(const void* gate_up, int d_ff, void* out, int rows, gllm_stream_t stream) {
   return silu_mul((const bf16*)gate_up, d_ff, (bf16*)out, rows, reinterpret_cast<cudaStream_t>(stream));
 }
+
+uint32_t gllm_meta_errors(int reset) { return meta_errors(reset); }
 
 int gllm_prepare_batch(const gllm_stage* stage, const gllm_batch* batch, int32_t* tok_pos, int32_t* tok_slot,
                        int32_t* tok_id, int32_t* emit_rows, gllm_stream_t stream) {

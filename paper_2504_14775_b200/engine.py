@@ -254,7 +254,10 @@ class EngineCore:
         self.kv: KvCacheState = PagedKvCache(kv_config) if executor is not None else KvCacheState(kv_config)
         self._rows_free: list[int] = []
         self._rows_next = 0
-        self._max_rows = max_rows if max_rows is not None else max(1, len(requests))
+        if max_rows is None:
+            max_rows = getattr(executor, "max_rows", None) or max(1, min(len(requests) or kv_config.total_pages,
+                                                                         kv_config.total_pages))
+        self._max_rows = max_rows
         self.clock = 0.0
         self.makespan_ms = 0.0
         self.committed_tokens = 0
@@ -275,6 +278,41 @@ class EngineCore:
         self._seq = 0
         self._pending_prompts: list[tuple[int, int]] = []
         self._ctx_log: dict[int, int] = {}   # seq -> decode context tokens (cost-model calibration)
+
+    # -- request intake ----------------------------------------------------------
+
+    def _validate_new(self, spec: RequestSpec) -> None:
+        if spec.id in self._reqs:
+            raise ConfigError(f"duplicate request id {spec.id}")
+        kvc = self.kv.config
+        need = pages_needed(0, spec.input_tokens + spec.output_tokens - 1, kvc.page_size)
+        if need > kvc.total_pages:
+            raise UnschedulableError(
+                f"request {spec.id} needs {need} KV pages over its lifetime "
+                f"but the cache has only {kvc.total_pages}", (spec.id,))
+        lim = getattr(self.executor, "max_seq_len", None)
+        if lim is not None and spec.input_tokens + spec.output_tokens + 1 > lim:
+            raise ConfigError(f"request {spec.id}: {spec.input_tokens}+{spec.output_tokens} tokens exceed "
+                              f"the executor's max_seq_len={lim}")
+
+    def _add_request(self, spec: RequestSpec, prompt_ids=None) -> _Req:
+        """Register a request (front-end submit, `PAPER.md:252`); its prompt tokens, if given, are
+        what the first stage embeds (else the seeded synthetic prompt of the trace format)."""
+        self._validate_new(spec)
+        if prompt_ids is not None:
+            import numpy as _np
+            ids = _np.asarray(prompt_ids, dtype=_np.int32).reshape(-1)
+            if ids.size != spec.input_tokens:
+                raise ConfigError(f"request {spec.id}: {ids.size} prompt ids for input_tokens={spec.input_tokens}")
+            if self.executor is None or not hasattr(self.executor, "register_prompt"):
+                raise ConfigError("prompt ids need a GPU executor")
+            self.executor.register_prompt(spec.id, ids)
+        if self.executor is not None and hasattr(self.executor, "add_request"):
+            self.executor.add_request(spec)
+        r = _Req(spec)
+        self._reqs[spec.id] = r
+        self._order.append(spec.id)
+        return r
 
     # -- logging ---------------------------------------------------------------
 
@@ -391,9 +429,19 @@ class EngineCore:
         stored = [toks[rid] for rid in chosen]   # decode-ready requests always hold KV
         reserved = sum(1 for s in stored if s % ps == 0)
 
+        paged = self.executor is not None
+        rows_left = len(self._rows_free) + self._max_rows - self._rows_next
+
         def cands():
+            nonlocal rows_left
             for _, rid in self._waiting:
                 r = reqs[rid]
+                if paged and r.row < 0:
+                    # a new request needs a block-table row; rows are bounded by concurrency, so
+                    # when none is free the FCFS fill stops here, as it does at a KV truncation
+                    if rows_left <= 0:
+                        return
+                    rows_left -= 1
                 yield rid, r.target - r.done, kv.stored_tokens(rid)
 
         chunks = fill_prefill(cands(), limit, free - reserved, ps)
@@ -406,8 +454,8 @@ class EngineCore:
         if self._rows_free:
             r.row = self._rows_free.pop()
         else:
-            if self._rows_next >= self._max_rows:
-                raise ConfigError(f"out of block-table rows (max_rows={self._max_rows})")
+            if self._rows_next >= self._max_rows:   # planning admits only as many new rows as are free
+                raise AssertionError(f"out of block-table rows (max_rows={self._max_rows})")
             r.row = self._rows_next
             self._rows_next += 1
         self.kv.bind_row(rid, r.row)
@@ -576,6 +624,14 @@ class Engine(EngineCore):
         self._unfinished = len(self._reqs)
         for rid in self._order:
             self._push(self._reqs[rid].spec.arrival_ms, _EV_ARRIVAL, rid, 0)
+
+    def submit(self, spec: RequestSpec, prompt_ids=None) -> None:
+        """Add a request at `spec.arrival_ms` (>= the engine clock) with optional real prompt ids."""
+        if spec.arrival_ms < self.clock:
+            raise ConfigError(f"request {spec.id} arrives at {spec.arrival_ms} ms, before the clock {self.clock}")
+        self._add_request(spec, prompt_ids)
+        self._unfinished += 1
+        self._push(spec.arrival_ms, _EV_ARRIVAL, spec.id, 0)
 
     def _push(self, t: float, kind: int, a: int, b: int) -> None:
         heapq.heappush(self._heap, (t, self._eseq, kind, a, b))

@@ -17,8 +17,10 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import native
 from .modelspec import ModelSpec, stage_layers
-from .stage import PackedBatch, StageWorker, default_prompt_source, pack_batch
+from .stage import (PackedBatch, StageWorker, default_max_rows, default_max_seq_len, pack_batch,
+                    prompt_source_with)
 
 
 class _PinnedRing:
@@ -58,14 +60,15 @@ class LocalExecutor:
     def __init__(self, spec: ModelSpec, requests, *, num_pages: int, page_size: int = 16, n_stages: int = 1,
                  max_rows: int | None = None, max_tokens: int = 4096, max_emit: int | None = None,
                  seed: int = 0, device="cuda", record_logits: bool = False, record_ids=None,
-                 ring_slots: int = 8):
+                 ring_slots: int = 8, max_seq_len: int | None = None):
         import torch
 
         self.spec = spec
         self.device = torch.device(device)
         self.specs = {r.id: r for r in requests}
-        max_rows = max_rows if max_rows is not None else max(1, len(requests))
-        max_seq_len = max(r.input_tokens + r.output_tokens for r in requests) + 1 if requests else 16
+        max_rows = max_rows if max_rows is not None else default_max_rows(requests, num_pages)
+        max_seq_len = max_seq_len if max_seq_len is not None else default_max_seq_len(requests)
+        self.max_rows, self.max_seq_len = max_rows, max_seq_len
         max_emit = max_emit if max_emit is not None else max(1, min(max_rows, max_tokens))
         self.max_tokens = max_tokens
         self.stages = [StageWorker(spec, stage_layers(spec.n_layers, n_stages, s), is_first=(s == 0),
@@ -73,7 +76,8 @@ class LocalExecutor:
                                    max_rows=max_rows, max_seq_len=max_seq_len, max_tokens=max_tokens,
                                    max_emit=max_emit, seed=seed, device=self.device) for s in range(n_stages)]
         self.q_tile = self.stages[0].q_tile
-        self.prompt_source = default_prompt_source(self.specs, spec.vocab)
+        self.prompts: dict[int, np.ndarray] = {}
+        self.prompt_source = prompt_source_with(self.prompts, self.specs, spec.vocab)
         self.stream = torch.cuda.Stream(device=self.device)
         n_ints = 16 * max_tokens + 8 * max_rows + 4 * max_seq_len
         self.ring = _PinnedRing(ring_slots, n_ints, self.device)
@@ -85,6 +89,7 @@ class LocalExecutor:
         self.logits_dev = (torch.empty((max_emit, spec.vocab), dtype=torch.bfloat16, device=self.device)
                            if record_logits else None)
         self._inflight: dict[int, tuple] = {}
+        self._done: dict[int, object] = {}                # seq -> batch-finished event (device windows)
         self.outputs: dict[int, list[int]] = {}          # request id -> sampled tokens, in order
         self.logits: list[tuple[int, int, np.ndarray]] = []  # (request id, position, fp32 logits)
         self.timings: list = []                           # (seq, [(start, end) event per stage])
@@ -134,12 +139,14 @@ class LocalExecutor:
             done.record(st)
         self.ring.fence(k, done)
         self._inflight[pb.seq] = (pb, done, host, logits_host)
+        self._done[pb.seq] = done
         self.timings.append((pb.seq, evs))
         self.launches += 1
 
     def retire(self, seq: int) -> list[int]:
         pb, done, host, logits_host = self._inflight.pop(seq)
         done.synchronize()
+        native.check_meta_errors()
         toks = host[:pb.n_emit].tolist()
         for rid, tok in zip(pb.emit_ids, toks):
             self.outputs.setdefault(rid, []).append(tok)
@@ -151,7 +158,13 @@ class LocalExecutor:
         return toks
 
     def on_finish(self, request_id: int, row: int) -> None:
-        pass
+        self.prompts.pop(request_id, None)
+
+    def register_prompt(self, request_id: int, tokens) -> None:
+        self.prompts[request_id] = np.asarray(tokens, dtype=np.int32)
+
+    def add_request(self, spec) -> None:
+        self.specs[spec.id] = spec
 
     # -- wall-clock driver hooks ------------------------------------------------------
 
@@ -175,6 +188,16 @@ class LocalExecutor:
         """seq -> device ms of the whole micro-batch (all stages), from CUDA events on the launch stream."""
         self.synchronize()
         return {seq: evs[0][0].elapsed_time(evs[-1][1]) for seq, evs in self.timings}
+
+    def device_window_ms(self, first: int, last: int) -> float:
+        """Device time from batch `first` starting to batch `last` finishing (gaps included)."""
+        self.synchronize()
+        start = next(evs[0][0] for s, evs in self.timings if s == first)
+        return start.elapsed_time(self._done[last])
+
+    def stage_busy_ms(self, first: int, last: int) -> float:
+        self.synchronize()
+        return sum(evs[0][0].elapsed_time(evs[-1][1]) for s, evs in self.timings if first <= s <= last)
 
     def h2d_bytes_total_for(self, seqs) -> int:
         return sum(self.h2d_bytes.get(s, 0) for s in seqs)

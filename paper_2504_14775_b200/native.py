@@ -24,8 +24,11 @@ EXPORTS = (
     "gllm_rmsnorm", "gllm_silu_mul",
     "gllm_prepare_batch", "gllm_embed", "gllm_rope_kv_write", "gllm_attn_mixed_paged", "gllm_attn_mixed_paged_split", "gllm_attn_mixed_paged_auto",
     "gllm_attn_split_workspace_bytes", "gllm_argmax",
-    "gllm_launch_count", "gllm_profile_begin", "gllm_profile_end",
+    "gllm_launch_count", "gllm_profile_begin", "gllm_profile_end", "gllm_meta_errors",
 )
+
+META_ERRORS = {1: "block-table delta out of range", 2: "prompt header out of range",
+               4: "sequence row / position out of range", 8: "token position maps to an invalid page"}
 
 
 class Dims(C.Structure):
@@ -98,6 +101,7 @@ def load() -> C.CDLL:
         "gllm_launch_count": (C.c_ulonglong, []),
         "gllm_profile_begin": (i, []),
         "gllm_profile_end": (i, [C.POINTER(ProfileEntry), i, C.POINTER(i)]),
+        "gllm_meta_errors": (C.c_uint32, [i]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -138,6 +142,14 @@ def profile_end() -> dict[str, dict]:
     call("gllm_profile_end", arr, 64, C.byref(n))
     return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
                                    "flops": arr[i].flops, "bytes": arr[i].bytes} for i in range(n.value)}
+
+
+def check_meta_errors() -> None:
+    """Raise if any micro-batch's metadata failed the device bounds checks (gllm_meta_errors)."""
+    v = int(load().gllm_meta_errors(1))
+    if v:
+        why = ", ".join(m for b, m in META_ERRORS.items() if v & b)
+        raise NativeError("gllm_meta_errors", v, f"device metadata bounds check failed: {why}")
 
 
 def launch_count() -> int:

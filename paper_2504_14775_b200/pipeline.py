@@ -33,20 +33,22 @@ from dataclasses import dataclass
 import numpy as np
 
 from .modelspec import ModelSpec, stage_layers
-from .stage import PackedBatch, StageWorker, default_prompt_source, pack_batch
+from .stage import (PackedBatch, StageWorker, default_max_rows, default_max_seq_len, pack_batch,
+                    prompt_source_with)
 
-HEADER = 9
+HEADER = 10
 STOP = -1
+FLAG_PROFILE = 1   # header flag: capture this batch with the native profiler on every rank
 
 
 def header_of(pb: PackedBatch) -> np.ndarray:
     return np.array([pb.seq, pb.n_seqs, pb.n_tokens, pb.n_emit, pb.n_work, pb.n_prefill_work, pb.n_deltas,
-                     pb.n_prompts, pb.data.size], dtype=np.int32)
+                     pb.n_prompts, pb.flags, pb.data.size], dtype=np.int32)
 
 
 def batch_from(header: np.ndarray, data: np.ndarray) -> PackedBatch:
-    seq, n_seqs, n_tokens, n_emit, n_work, n_pf, n_deltas, n_prompts, _ = (int(x) for x in header)
-    return PackedBatch(seq, n_seqs, n_tokens, n_emit, n_work, n_pf, n_deltas, n_prompts, data, [], [])
+    seq, n_seqs, n_tokens, n_emit, n_work, n_pf, n_deltas, n_prompts, flags, _ = (int(x) for x in header)
+    return PackedBatch(seq, n_seqs, n_tokens, n_emit, n_work, n_pf, n_deltas, n_prompts, data, [], [], flags)
 
 
 # ------------------------------------------------------------------ transports
@@ -174,21 +176,50 @@ class _null:
 class _Flight:
     pb: PackedBatch
     fwd_done: object      # CUDA event: stage-0 forward finished (stage 0 free again)
-    done: object          # CUDA event: sampled tokens on the host
+    done: object          # CUDA event: sampled tokens committed to the history and copied to the host
     host: object
+
+
+class _PinnedSlots:
+    """Pinned host staging for the metadata of the last `n` micro-batches (H2D copies stay async):
+    slot k is rewritten only after the copy that last read it (event) has run."""
+
+    def __init__(self, n: int, n_ints: int, pinned: bool):
+        import torch
+
+        self.pinned = pinned
+        self.host = [torch.empty(n_ints, dtype=torch.int32, pin_memory=pinned) for _ in range(n)]
+        self.read = [None] * n
+
+    def stage(self, k: int, data: np.ndarray):
+        import torch
+
+        if self.read[k] is not None:
+            self.read[k].synchronize()
+        if data.size > self.host[k].numel():
+            self.host[k] = torch.empty(2 * data.size, dtype=torch.int32, pin_memory=self.pinned)
+        self.host[k][: data.size].numpy()[:] = data
+        return self.host[k][: data.size]
 
 
 class PipelineExecutor:
     """Executor protocol (see executor.py) for rank 0 of a PP=world pipeline.
 
-    Rank 0 holds stage 0 and the token history; it publishes each launched
-    micro-batch's metadata, runs stage 0, sends the activations to rank 1 and
-    posts the receive of the sampled ids from the last rank.
+    Rank 0 holds stage 0 and the token history; it publishes each launched micro-batch's
+    metadata, runs stage 0 on the compute stream, sends the activations to rank 1 on the send
+    stream and receives the sampled ids from the last rank on the recv stream, where they are
+    also committed into the token history and copied to the host. Nothing on the compute stream
+    waits for a batch's own round trip: batch b's forward waits only for
+      * the sampled ids of batch b - `lag` (the newest batch whose commit the scheduler had
+        applied when it planned b: `lag` = depth, see ServingEngine lookahead), and
+      * the send / token receive of batch b - ring (ring slot k = b % ring is reused).
+    so stage 0 runs batch b+1 while b is on later stages (inter-batch overlap, `PAPER.md:258-263`).
     """
 
     def __init__(self, spec: ModelSpec, requests, *, world: int, meta: MetaChannel, transport, num_pages: int,
                  page_size: int = 16, max_tokens: int = 4096, max_emit: int | None = None, seed: int = 0,
-                 device="cuda", stage_factory=None, ring: int = 8):
+                 device="cuda", stage_factory=None, ring: int = 8, max_rows: int | None = None,
+                 max_seq_len: int | None = None, lag: int | None = None):
         import torch
 
         self.spec = spec
@@ -197,81 +228,112 @@ class PipelineExecutor:
         self.transport = transport
         self.device = torch.device(device)
         self.specs = {r.id: r for r in requests}
-        max_rows = max(1, len(requests))
-        max_seq_len = max(r.input_tokens + r.output_tokens for r in requests) + 1 if requests else 16
+        max_rows = max_rows if max_rows is not None else default_max_rows(requests, num_pages)
+        max_seq_len = max_seq_len if max_seq_len is not None else default_max_seq_len(requests)
         self.max_emit = max_emit if max_emit is not None else max(1, min(max_rows, max_tokens))
         factory = stage_factory or StageWorker
         self.stage = factory(spec, stage_layers(spec.n_layers, world, 0), is_first=True, is_last=(world == 1),
                              num_pages=num_pages, page_size=page_size, max_rows=max_rows, max_seq_len=max_seq_len,
                              max_tokens=max_tokens, max_emit=self.max_emit, seed=seed, device=self.device)
         self.q_tile = self.stage.q_tile
-        self.prompt_source = default_prompt_source(self.specs, spec.vocab)
+        self.prompts: dict[int, np.ndarray] = {}
+        self.prompt_source = prompt_source_with(self.prompts, self.specs, spec.vocab)
         on_gpu = self.device.type == "cuda"
+        self.on_gpu = on_gpu
         self.compute = torch.cuda.Stream(device=self.device) if on_gpu else None
         # separate streams: activations out to rank 1 must not queue behind the token
         # receive from the last rank (different peers, independent progress)
         self.send_stream = torch.cuda.Stream(device=self.device) if on_gpu else None
         self.recv_stream = torch.cuda.Stream(device=self.device) if on_gpu else None
+        if ring < world + 2:
+            raise ValueError(f"ring={ring} must be >= world + 2 (batches in flight + one queued)")
         self.ring = ring
+        self.lag = lag if lag is not None else world
+        n_ints = 16 * max_tokens + 8 * max_rows + 4 * max_seq_len
         self.hidden = [torch.empty((max_tokens, spec.d_model), dtype=torch.bfloat16, device=self.device)
                        for _ in range(ring)]
         self.sampled = [torch.empty(self.max_emit, dtype=torch.int32, device=self.device) for _ in range(ring)]
         self.sampled_host = [torch.empty(self.max_emit, dtype=torch.int32, pin_memory=on_gpu) for _ in range(ring)]
-        self.meta_dev = [torch.empty(16 * max_tokens + 8 * max_rows + 4 * max_seq_len, dtype=torch.int32,
-                                     device=self.device) for _ in range(ring)]
+        self.meta_dev = [torch.empty(n_ints, dtype=torch.int32, device=self.device) for _ in range(ring)]
+        self.staging = _PinnedSlots(ring, n_ints, on_gpu)
+        self._slot_free = [None] * ring      # event: slot k's send + token commit of its last batch done
+        self._tok_done: dict[int, object] = {}
         self._inflight: dict[int, _Flight] = {}
+        self._done: dict[int, object] = {}   # seq -> tokens-committed event (device windows)
         self._last_fwd = None
         self.outputs: dict[int, list[int]] = {}
         self.timings: list = []
         self._epoch = None
         self.launches = 0
+        self.publish_flags = 0
         self.h2d_bytes: dict[int, int] = {}
         if on_gpu:
             torch.cuda.synchronize(self.device)
 
     def _event(self):
         import torch
-        return torch.cuda.Event(enable_timing=True) if self.device.type == "cuda" else _HostEvent()
+        return torch.cuda.Event(enable_timing=True) if self.on_gpu else _HostEvent()
+
+    def _record(self, ev, stream):
+        ev.record(stream) if stream is not None else ev.record()
+        return ev
+
+    def register_prompt(self, request_id: int, tokens) -> None:
+        self.prompts[request_id] = np.asarray(tokens, dtype=np.int32)
+
+    def add_request(self, spec) -> None:
+        self.specs[spec.id] = spec
 
     def launch(self, meta) -> None:
         import torch
 
         pb = pack_batch(meta, self.q_tile, self.prompt_source)
-        k = pb.seq % self.ring
+        pb.flags = self.publish_flags
+        seq, k = pb.seq, pb.seq % self.ring
         self.meta.publish(pb)                         # metadata ahead of activations
         md = self.meta_dev[k]
         if pb.data.size > md.numel():
             self.meta_dev[k] = md = torch.empty(2 * pb.data.size, dtype=torch.int32, device=self.device)
-        src = torch.from_numpy(pb.data)
-        self.h2d_bytes[pb.seq] = int(pb.data.nbytes)
+        staged = self.staging.stage(k, pb.data)
+        self.h2d_bytes[seq] = int(pb.data.nbytes)
         a, b = self._event(), self._event()
         with _on(self.compute):
-            md[: pb.data.size].copy_(src.pin_memory() if self.device.type == "cuda" else src, non_blocking=True)
-            a.record(self.compute) if self.compute is not None else a.record()
+            if self.on_gpu:
+                if self._slot_free[k] is not None:        # batch seq - ring released slot k
+                    self.compute.wait_event(self._slot_free[k])
+                dep = self._tok_done.pop(seq - self.lag, None)
+                if dep is not None:                       # decode inputs sampled by batch seq - lag
+                    self.compute.wait_event(dep)
+            md[: pb.data.size].copy_(staged, non_blocking=True)
+            self.staging.read[k] = self._record(self._event(), self.compute)
+            self._record(a, self.compute)
             self.stage.forward(pb, md, hidden=self.hidden[k], sampled=self.sampled[k], stream=self.compute)
-            b.record(self.compute) if self.compute is not None else b.record()
+            self._record(b, self.compute)
         host = self.sampled_host[k]
         if self.world > 1:
-            if self.send_stream is not None:
+            if self.on_gpu:
                 self.send_stream.wait_event(b)
             self.transport.send(self.hidden[k][: pb.n_tokens], 1, self.send_stream)
-            if pb.n_emit:
-                self.transport.recv(self.sampled[k][: pb.n_emit], self.world - 1, self.recv_stream)
-                with _on(self.compute):
-                    if self.compute is not None:
-                        self.compute.wait_stream(self.recv_stream)
-                    self.stage.commit_tokens(pb, md, self.sampled[k], stream=self.compute)
-            # the next use of hidden[k] (batch seq+ring) must follow this send
-            if self.compute is not None:
-                self.compute.wait_stream(self.send_stream)
-        with _on(self.compute):
-            if pb.n_emit:
-                host[: pb.n_emit].copy_(self.sampled[k][: pb.n_emit], non_blocking=True)
-            done = self._event()
-            done.record(self.compute) if self.compute is not None else done.record()
-        self._inflight[pb.seq] = _Flight(pb, b, done, host)
+            sent = self._record(self._event(), self.send_stream)
+            with _on(self.recv_stream):
+                if self.on_gpu:
+                    self.recv_stream.wait_event(sent)     # slot k free only after both
+                if pb.n_emit:
+                    self.transport.recv(self.sampled[k][: pb.n_emit], self.world - 1, self.recv_stream)
+                    self.stage.commit_tokens(pb, md, self.sampled[k], stream=self.recv_stream)
+                    host[: pb.n_emit].copy_(self.sampled[k][: pb.n_emit], non_blocking=True)
+                done = self._record(self._event(), self.recv_stream)
+        else:
+            with _on(self.compute):
+                if pb.n_emit:
+                    host[: pb.n_emit].copy_(self.sampled[k][: pb.n_emit], non_blocking=True)
+                done = self._record(self._event(), self.compute)
+        self._slot_free[k] = done
+        self._tok_done[seq] = done
+        self._done[seq] = done
+        self._inflight[seq] = _Flight(pb, b, done, host)
         self._last_fwd = b
-        self.timings.append((pb.seq, [(a, b)]))
+        self.timings.append((seq, [(a, b)]))
         self.launches += 1
 
     def stage0_idle(self) -> bool:
@@ -283,17 +345,19 @@ class PipelineExecutor:
     def retire(self, seq: int) -> list[int]:
         f = self._inflight.pop(seq)
         f.done.synchronize()
+        if self.on_gpu:
+            from . import native
+            native.check_meta_errors()
         toks = f.host[: f.pb.n_emit].tolist()
         for rid, tok in zip(f.pb.emit_ids, toks):
             self.outputs.setdefault(rid, []).append(tok)
         return toks
 
     def on_finish(self, request_id: int, row: int) -> None:
-        pass
+        self.prompts.pop(request_id, None)
 
     def mark_epoch(self) -> None:
-        self._epoch = self._event()
-        self._epoch.record(self.compute) if self.compute is not None else self._epoch.record()
+        self._epoch = self._record(self._event(), self.compute)
         self.timings.clear()
 
     def synchronize(self) -> None:
@@ -312,6 +376,17 @@ class PipelineExecutor:
         self.synchronize()
         return {seq: a.elapsed_time(b) for seq, ((a, b),) in self.timings}
 
+    def device_window_ms(self, first: int, last: int) -> float:
+        """Device time from stage 0 starting batch `first` to batch `last`'s sampled tokens being
+        committed (they return from the last stage): the pipeline's whole span on this GPU."""
+        self.synchronize()
+        start = next(a for s, ((a, _),) in self.timings if s == first)
+        return start.elapsed_time(self._done[last])
+
+    def stage_busy_ms(self, first: int, last: int) -> float:
+        self.synchronize()
+        return sum(a.elapsed_time(b) for s, ((a, b),) in self.timings if first <= s <= last)
+
     def h2d_bytes_total_for(self, seqs) -> int:
         return sum(self.h2d_bytes.get(s, 0) for s in seqs)
 
@@ -325,65 +400,102 @@ class PipelineExecutor:
 
 def worker_loop(spec: ModelSpec, requests, *, rank: int, world: int, meta: MetaChannel, transport, num_pages: int,
                 page_size: int = 16, max_tokens: int = 4096, max_emit: int | None = None, seed: int = 0,
-                device="cuda", stage_factory=None, ring: int = 8) -> dict:
-    """Run stage `rank` until the driver publishes STOP; returns busy intervals (ms since start)."""
+                device="cuda", stage_factory=None, ring: int = 8, max_rows: int | None = None,
+                max_seq_len: int | None = None, stage=None) -> dict:
+    """Run stage `rank` until the driver publishes STOP; returns per-batch CUDA-event spans.
+
+    The host loop never waits on the device except to reuse a pinned metadata slot (ring
+    batches back): metadata is received on the CPU group, staged in pinned memory and copied
+    asynchronously; the activation receive (recv stream) and the send (send stream) are ordered
+    against the forward by events.
+    """
     import torch
 
     dev = torch.device(device)
-    max_rows = max(1, len(requests))
-    max_seq_len = max(r.input_tokens + r.output_tokens for r in requests) + 1 if requests else 16
+    max_rows = max_rows if max_rows is not None else default_max_rows(requests, num_pages)
+    max_seq_len = max_seq_len if max_seq_len is not None else default_max_seq_len(requests)
     max_emit = max_emit if max_emit is not None else max(1, min(max_rows, max_tokens))
-    factory = stage_factory or StageWorker
-    stage = factory(spec, stage_layers(spec.n_layers, world, rank), is_first=False, is_last=(rank == world - 1),
-                    num_pages=num_pages, page_size=page_size, max_rows=max_rows, max_seq_len=max_seq_len,
-                    max_tokens=max_tokens, max_emit=max_emit, seed=seed, device=dev)
+    if stage is None:
+        factory = stage_factory or StageWorker
+        stage = factory(spec, stage_layers(spec.n_layers, world, rank), is_first=False, is_last=(rank == world - 1),
+                        num_pages=num_pages, page_size=page_size, max_rows=max_rows, max_seq_len=max_seq_len,
+                        max_tokens=max_tokens, max_emit=max_emit, seed=seed, device=dev)
     on_gpu = dev.type == "cuda"
     compute = torch.cuda.Stream(device=dev) if on_gpu else None
     recv_s = torch.cuda.Stream(device=dev) if on_gpu else None
     send_s = torch.cuda.Stream(device=dev) if on_gpu else None
+    n_ints = 16 * max_tokens + 8 * max_rows + 4 * max_seq_len
     hidden = [torch.empty((max_tokens, spec.d_model), dtype=torch.bfloat16, device=dev) for _ in range(ring)]
     sampled = [torch.empty(max_emit, dtype=torch.int32, device=dev) for _ in range(ring)]
-    meta_dev = torch.empty(16 * max_tokens + 8 * max_rows + 4 * max_seq_len, dtype=torch.int32, device=dev)
+    meta_dev = [torch.empty(n_ints, dtype=torch.int32, device=dev) for _ in range(ring)]
+    staging = _PinnedSlots(ring, n_ints, on_gpu)
+    sent = [None] * ring
+    mk = (lambda: torch.cuda.Event(enable_timing=True)) if on_gpu else _HostEvent
     if on_gpu:
         torch.cuda.synchronize(dev)
-    epoch = torch.cuda.Event(enable_timing=True) if on_gpu else _HostEvent()
+    epoch = mk()
     epoch.record(compute) if on_gpu else epoch.record()
-    spans = []
+    spans = {}
     n = 0
+    profiling, profile = False, None
+    from . import native as _native
     while True:
         pb = meta.receive()
         if pb is None:
             break
+        if on_gpu and bool(pb.flags & FLAG_PROFILE) != profiling:
+            if profiling:                   # the profiled window ended with the previous batch
+                torch.cuda.synchronize(dev)
+                profile = _native.profile_end()
+            else:
+                _native.profile_begin()
+            profiling = not profiling
         k = pb.seq % ring
-        if pb.data.size > meta_dev.numel():
-            meta_dev = torch.empty(2 * pb.data.size, dtype=torch.int32, device=dev)
-        with _on(compute):
-            meta_dev[: pb.data.size].copy_(torch.from_numpy(pb.data), non_blocking=False)
-        if on_gpu:
-            recv_s.wait_stream(send_s)        # slot k's previous send has drained
-        transport.recv(hidden[k][: pb.n_tokens], rank - 1, recv_s)
-        a = torch.cuda.Event(enable_timing=True) if on_gpu else _HostEvent()
-        b = torch.cuda.Event(enable_timing=True) if on_gpu else _HostEvent()
+        md = meta_dev[k]
+        if pb.data.size > md.numel():
+            meta_dev[k] = md = torch.empty(2 * pb.data.size, dtype=torch.int32, device=dev)
+        staged = staging.stage(k, pb.data)
+        with _on(recv_s):
+            if on_gpu and sent[k] is not None:
+                recv_s.wait_event(sent[k])        # slot k's previous send has drained
+            transport.recv(hidden[k][: pb.n_tokens], rank - 1, recv_s)
+            got = mk()
+            got.record(recv_s) if on_gpu else got.record()
+        a, b = mk(), mk()
         with _on(compute):
             if on_gpu:
-                compute.wait_stream(recv_s)
-                a.record(compute)
-            else:
-                a.record()
-            stage.forward(pb, meta_dev, hidden=hidden[k], sampled=sampled[k], stream=compute)
+                compute.wait_event(got)
+            md[: pb.data.size].copy_(staged, non_blocking=True)
+            rd = mk()
+            rd.record(compute) if on_gpu else rd.record()
+            staging.read[k] = rd
+            a.record(compute) if on_gpu else a.record()
+            stage.forward(pb, md, hidden=hidden[k], sampled=sampled[k], stream=compute)
             b.record(compute) if on_gpu else b.record()
-        if on_gpu:
-            send_s.wait_event(b)
-        if rank == world - 1:
-            if pb.n_emit:
-                transport.send(sampled[k][: pb.n_emit], 0, send_s)
-        else:
-            transport.send(hidden[k][: pb.n_tokens], rank + 1, send_s)
-        spans.append((a, b))
+        with _on(send_s):
+            if on_gpu:
+                send_s.wait_event(b)
+            if rank == world - 1:
+                if pb.n_emit:
+                    transport.send(sampled[k][: pb.n_emit], 0, send_s)
+            else:
+                transport.send(hidden[k][: pb.n_tokens], rank + 1, send_s)
+            ev = mk()
+            ev.record(send_s) if on_gpu else ev.record()
+            sent[k] = ev
+        spans[pb.seq] = (a, b)
         n += 1
+        if on_gpu:
+            from . import native
+            native.check_meta_errors()    # host-mapped flag: no sync (reports a violation a batch late)
     if on_gpu:
         torch.cuda.synchronize(dev)
-    return {"batches": n, "busy": [(epoch.elapsed_time(a), epoch.elapsed_time(b)) for a, b in spans]}
+        from . import native
+        native.check_meta_errors()
+        if profiling:
+            profile = native.profile_end()
+    return {"batches": n, "profile": profile, "busy": [(epoch.elapsed_time(a), epoch.elapsed_time(b)) for a, b in spans.values()],
+            "spans": {seq: (epoch.elapsed_time(a), epoch.elapsed_time(b)) for seq, (a, b) in spans.items()}}
 
 
 class _on:
@@ -423,143 +535,3 @@ class _HostEvent:
 
     def elapsed_time(self, other):
         return (other.t - self.t) * 1000.0
-
-
-# ------------------------------------------------------------------ bench entry (torchrun, N > 1)
-
-
-def _bubble(busy) -> float:
-    """Idle fraction of one stage between its first start and last end (CUDA-event busy intervals;
-    the reference's per-stage bubble definition, `engine.py:108-125`, over the measured run)."""
-    if not busy:
-        return 0.0
-    t0 = min(a for a, _ in busy)
-    t1 = max(b for _, b in busy)
-    return 1.0 - sum(b - a for a, b in busy) / max(t1 - t0, 1e-9)
-
-
-def bench_pipeline(args) -> int:
-    """`bench.py --gpus N` under torchrun: PP=N over the same model and trace (strong scaling)."""
-    import json
-    import statistics
-
-    import torch
-    import torch.distributed as dist
-
-    from . import KvConfig, PipelineConfig, ThrottleConfig, build_report
-    from .modelspec import MODELS
-    from .serving import ServingEngine
-    from .workload import ArrivalProcess, builtin_length_table, synthesize_requests
-
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    dev_id = local % torch.cuda.device_count()
-    torch.cuda.set_device(dev_id)
-    # GLLM_PP_TRANSPORT=host: activations staged through host memory over gloo (lets all ranks
-    # share one GPU for testing); default: NCCL send/recv between the ranks' GPUs.
-    host_transport = os.environ.get("GLLM_PP_TRANSPORT", "nccl") == "host"
-    if host_transport:
-        dist.init_process_group("gloo")
-        gloo = dist.group.WORLD
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_id))
-        gloo = dist.new_group(backend="gloo")
-    spec = MODELS[args.model]
-    reqs = synthesize_requests(ArrivalProcess.poisson(args.rate, 0), builtin_length_table("sharegpt-like"),
-                               args.n_requests)
-    page_size = 16
-    max_tokens = (2048 + args.n_requests + 255) // 256 * 256
-    layers = len(stage_layers(spec.n_layers, world, 0))
-    need_pages = sum(-(-(r.input_tokens + r.output_tokens) // page_size) for r in reqs)
-    free, _ = torch.cuda.mem_get_info()
-    free //= max(1, sum(1 for r in range(world) if r % torch.cuda.device_count() == dev_id))  # shared GPU
-    w_bytes = layers * spec.params_per_layer * 2 + 2 * spec.vocab * spec.d_model * 2
-    page_bytes = layers * spec.kv_bytes_per_token_layer * page_size
-    fit = int((free - w_bytes - max_tokens * (10 * spec.d_model + 6 * spec.d_ff) * 2 * 4 - (10 << 30)) // page_bytes)
-    num_pages = torch.tensor([max(1024, min(need_pages, fit))], dtype=torch.int64)
-    dist.all_reduce(num_pages, op=dist.ReduceOp.MIN, group=gloo)   # one shared page table: same pool size
-    num_pages = int(num_pages.item())
-    meta = MetaChannel(gloo, world)
-    transport = HostTransport(gloo) if host_transport else NcclTransport(rank, make_links(world))
-    from . import native
-    launches0 = native.launch_count()
-    dist.barrier(group=gloo)
-    if rank != 0:
-        out = worker_loop(spec, reqs, rank=rank, world=world, meta=meta, transport=transport, num_pages=num_pages,
-                          page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests,
-                          device=f"cuda:{dev_id}")
-        # per-batch launches of this stage (the timed window is only known to rank 0)
-        stats = torch.tensor([0.0, (native.launch_count() - launches0) / max(out["batches"], 1), 0.0],
-                             dtype=torch.float64)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=gloo)
-        bub = torch.zeros(world, dtype=torch.float64)
-        bub[rank] = _bubble(out["busy"])
-        dist.all_reduce(bub, op=dist.ReduceOp.SUM, group=gloo)
-        dist.destroy_process_group()
-        return 0
-    ex = PipelineExecutor(spec, reqs, world=world, meta=meta, transport=transport, num_pages=num_pages,
-                          page_size=page_size, max_tokens=max_tokens, max_emit=args.n_requests,
-                          device=f"cuda:{dev_id}")
-    eng = ServingEngine(reqs, scheduler=args.scheduler, pipeline=PipelineConfig(depth=world),
-                        kv_config=KvConfig(num_pages, page_size), throttle=ThrottleConfig(), executor=ex)
-    st = {"phase": "warm", "n": 0, "timed": []}
-    W, K = args.warmup, args.steps
-
-    class _Stop(Exception):
-        pass
-
-    def hook(seq, t, n_out):
-        if st["phase"] == "warm":
-            st["n"] += 1
-            if eng._rd >= args.warm_decodes or st["n"] >= args.warm_max_iters:
-                st["phase"], st["c"] = "warmup", 0
-        elif st["phase"] == "warmup":
-            st["c"] += 1
-            if st["c"] >= W:
-                st["phase"], st["t0"] = "timed", time.perf_counter()
-        else:
-            st["timed"].append((seq, t, n_out))
-            if len(st["timed"]) >= K:
-                st["t1"] = time.perf_counter()
-                raise _Stop
-
-    from bench import ClockSampler
-    clocks = ClockSampler(dev_id)
-    clocks.start()
-    try:
-        eng.run(on_commit=hook)
-    except _Stop:
-        pass
-    clk = clocks.stop()
-    ex.shutdown()
-    # rank 0's driver clock spans every stage of every timed batch (a batch commits only after
-    # the last rank's tokens arrive), so it is the max over ranks of the pipeline's time.
-    stats = torch.tensor([st["t1"] - st["t0"], (native.launch_count() - launches0) / max(ex.launches, 1), 0.0],
-                         dtype=torch.float64)
-    dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=gloo)
-    bub = torch.zeros(world, dtype=torch.float64)
-    bub[0] = _bubble(ex.stage_busy_intervals()[0])
-    dist.all_reduce(bub, op=dist.ReduceOp.SUM, group=gloo)
-    wall = stats[0:1]
-    out_tok = sum(n for _, _, n in st["timed"])
-    raw = eng.raw_data()
-    rep = build_report(raw)
-    line = {"metric": "output_tokens_per_s", "value": round(out_tok / wall.item(), 2), "unit": "tokens/s",
-            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": round(wall.item() * 1000 / K, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (random-init weights, seeded ShareGPT-like trace)",
-            "config": {"workload": f"{args.model} PP={world}, ShareGPT-like Poisson {args.rate}/s x {args.n_requests}",
-                       "model": args.model, "parallelism": f"pp{world}"},
-            "e2e": {"value": round(out_tok / wall.item(), 2), "unit": "tokens/s",
-                    "h2d_bytes_per_step": int(ex.h2d_bytes_total_for([s for s, _, _ in st["timed"]]) / max(K, 1)),
-                    "d2h_bytes_per_step": int(4 * out_tok / max(K, 1))},
-            "gpu_launches": int(round(stats[1].item() * K)),  # sum over stages of launches per batch x K
-            "clocks": clk,
-            "transport": "host-staged gloo (test)" if host_transport else "nccl p2p",
-            "serving": {"p50_ttft_ms": rep.ttft_p50_ms, "p50_tpot_ms": rep.tpot_p50_ms,
-                        "bubble_frac_per_stage": [round(float(b), 4) for b in bub.tolist()],
-                        "decodes_per_step": statistics.mean(eng._iters[s].decode_tokens for s, _, _ in st["timed"])}}
-    print(json.dumps(line))
-    dist.destroy_process_group()
-    return 0

@@ -18,6 +18,8 @@ the reference planner.
 from __future__ import annotations
 
 import time
+from bisect import bisect_left
+from collections import deque
 
 from .engine import EngineCore, PipelineConfig, RawRunData
 from .errors import UnschedulableError
@@ -35,6 +37,7 @@ class ServingEngine(EngineCore):
             raise ValueError("ServingEngine needs a GPU executor")
         super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget, executor, max_rows)
         self._arrivals = sorted(requests, key=lambda s: (s.arrival_ms, s.id))
+        self._arrival_keys = [(s.arrival_ms, s.id) for s in self._arrivals]
         self._next_arrival = 0
         self._time_scale = time_scale
         self._t0 = None
@@ -43,10 +46,30 @@ class ServingEngine(EngineCore):
         self.commit_log: list[tuple[int, float, int]] = []   # (seq, commit wall ms, sampled tokens)
         self.launch_log: list[tuple[int, float]] = []        # (seq, launch wall ms)
         self._lookahead = lookahead
-        self._pending: list[tuple] = []   # lookahead: (batch, first-token ids, finished ids) awaiting the device
+        self._pending: deque = deque()      # lookahead: launched batches the device has not retired
+        self._uncommitted: deque = deque()  # lookahead: launched batches whose commit is not applied yet
 
     def now_ms(self) -> float:
+        if self._t0 is None:
+            return 0.0
         return (time.perf_counter() - self._t0) * 1000.0 * self._time_scale
+
+    def submit(self, spec, prompt_ids=None) -> None:
+        """Front-end request intake (`PAPER.md:252`): the request arrives at `spec.arrival_ms` on the
+        serving clock (ms since `run` started; pass `now_ms()` for "now"), optionally with its real
+        prompt token ids. Safe to call before `run` or from `on_commit` callbacks during it."""
+        self._add_request(spec, prompt_ids)
+        self._unfinished += 1
+        key = (spec.arrival_ms, spec.id)
+        i = len(self._arrivals)
+        if self._arrival_keys and key < self._arrival_keys[-1]:
+            i = max(bisect_left(self._arrival_keys, key), self._next_arrival)
+        self._arrivals.insert(i, spec)
+        self._arrival_keys.insert(i, key)
+
+    def outputs(self, request_id: int) -> list[int]:
+        """Sampled token ids of a request so far (retired micro-batches only)."""
+        return list(getattr(self.executor, "outputs", {}).get(request_id, []))
 
     def _release_arrivals(self, t: float) -> None:
         arr = self._arrivals
@@ -118,17 +141,36 @@ class ServingEngine(EngineCore):
     # -- asynchronous scheduling -------------------------------------------------------
     #
     # Scheduling never reads token values (termination is by output count,
-    # `engine.py:343`), and a batch's device work depends on the previous batch only
-    # through device memory written in stream order (sampled ids -> token history, KV
-    # pages). So right after launching batch i the host can apply batch i's commit to
-    # the request state, plan batch i+1 and enqueue it behind i: the GPU never idles on
-    # host planning. Times are stamped when the device actually finishes a batch.
-    # Every plan is still a Token Throttling decision on the state it saw (decision-
-    # replay parity holds); with lookahead off the loop waits for each commit instead.
+    # `engine.py:343`), and a batch's device work depends on earlier batches only through
+    # device memory written in stream order (sampled ids -> token history, KV pages). In the
+    # reference at depth D, batch b is planned right after batch b-D commits, with batches
+    # b-D+1..b-1 still in flight (`engine.py:391-398`). So right after launching batch b-1 the
+    # host can apply batch b-D's commit to the request state (FIFO of D launched batches),
+    # plan batch b and enqueue it: the plan sees exactly the state the reference would, and the
+    # device orders b's forward after b-D's sampled tokens (executor `lag` = D). At D = 1 this
+    # is "commit i right after launching it, plan i+1". Times are stamped when the device
+    # actually finishes a batch; with lookahead off the loop waits for each commit instead.
+
+    def _state_commit(self, t: float) -> None:
+        """Apply the oldest uncommitted batch's commit to the request state (provisional times)."""
+        entry = self._uncommitted.popleft()
+        batch = entry["batch"]
+        ids = batch.meta.ids if batch.meta is not None else \
+            batch.plan.decode_ids + [r for r, _ in batch.plan.prefill_chunks]
+        reqs = self._reqs
+        no_first = [rid for rid in ids if reqs[rid].first_ms is None]
+        no_finish = [rid for rid in ids if reqs[rid].finish_ms is None]
+        self._commit(t, batch, retire=False)
+        entry["firsts"] = [rid for rid in no_first if reqs[rid].first_ms is not None]
+        entry["done"] = [rid for rid in no_finish if reqs[rid].finish_ms is not None]
+        entry["committed"] = True
 
     def _launch_ahead(self, t: float) -> bool:
-        if len(self._pending) > self._pipeline.depth or not self.executor.stage0_idle():
+        depth = self._pipeline.depth
+        if len(self._pending) > depth:
             return False
+        if self._uncommitted and len(self._uncommitted) >= depth:
+            self._state_commit(t)
         snap = self._decision_snapshot() if self.decisions is not None else None
         plan = self._try_plan()
         if plan is None:
@@ -138,14 +180,11 @@ class ServingEngine(EngineCore):
             self.decisions.append((batch.seq, snap, list(plan.decode_ids), list(plan.prefill_chunks)))
         self.executor.launch(batch.meta)
         self.launch_log.append((batch.seq, t))
-        ids = batch.meta.ids if batch.meta is not None else plan.decode_ids + [r for r, _ in plan.prefill_chunks]
-        reqs = self._reqs
-        no_first = [rid for rid in ids if reqs[rid].first_ms is None]
-        no_finish = [rid for rid in ids if reqs[rid].finish_ms is None]
-        self._commit(t, batch, retire=False)          # state only; provisional times
-        firsts = [rid for rid in no_first if reqs[rid].first_ms is not None]
-        done = [rid for rid in no_finish if reqs[rid].finish_ms is not None]
-        self._pending.append((batch, firsts, done))
+        entry = {"batch": batch, "committed": False, "firsts": [], "done": []}
+        self._pending.append(entry)
+        self._uncommitted.append(entry)
+        if depth == 1:
+            self._state_commit(t)     # nothing else can be in flight: plan the next batch now
         return True
 
     def _run_lookahead(self, max_commits, on_commit) -> RawRunData:
@@ -159,15 +198,19 @@ class ServingEngine(EngineCore):
             if self._unfinished > 0 and self._launch_ahead(t):
                 continue
             if self._pending:
-                batch, firsts, done = self._pending.pop(0)
+                entry = self._pending[0]
+                batch = entry["batch"]
                 ex.wait(batch.seq)
                 ex.retire(batch.seq)
                 t = self.now_ms()
                 self.clock = t
                 self.makespan_ms = max(self.makespan_ms, t)
-                for rid in firsts:
+                if not entry["committed"]:       # nothing newer was planned: commit on completion
+                    self._state_commit(t)
+                self._pending.popleft()
+                for rid in entry["firsts"]:
                     self._reqs[rid].first_ms = t
-                for rid in done:
+                for rid in entry["done"]:
                     self._reqs[rid].finish_ms = t
                 n_out = batch.meta.n_emit
                 self.commit_log.append((batch.seq, t, n_out))

@@ -41,6 +41,7 @@ class PackedBatch:
     data: np.ndarray             # int32 packed metadata (host)
     emit_ids: list[int]          # request id of each sampled row
     emit_pos: list[int]          # token position each sampled row predicts
+    flags: int = 0               # runtime flags carried in the PP metadata header (bit 0: profile)
 
 
 def pack_batch(meta, q_tile: int, prompt_source) -> PackedBatch:
@@ -125,7 +126,8 @@ class StageWorker:
         self.k_cache = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
         self.v_cache = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
         self.max_pages_per_row = -(-max_seq_len // page_size)
-        self.block_table = torch.zeros((max_rows, self.max_pages_per_row), dtype=torch.int32, device=dev)
+        # -1 = unmapped: a position whose page was never delivered fails the device bounds check
+        self.block_table = torch.full((max_rows, self.max_pages_per_row), -1, dtype=torch.int32, device=dev)
         self.token_hist = torch.zeros((max_rows, max_seq_len), dtype=torch.int32, device=dev) if is_first else None
         self.rope = torch.from_numpy(rope_table(spec, max_seq_len)).to(dev)
         self.dims = native.Dims(L, spec.d_model, spec.n_heads, spec.n_kv_heads, spec.head_dim, spec.d_ff, spec.vocab,
@@ -183,7 +185,31 @@ class StageWorker:
 
 
 def default_prompt_source(specs_by_id: dict, vocab: int):
+    """Seeded synthetic prompts (PCG64(1000 + id), or the trace's `token_seed`)."""
     def src(rid: int) -> np.ndarray:
         r = specs_by_id[rid]
         return prompt_token_ids(rid, r.input_tokens, vocab, getattr(r, "token_seed", None))
     return src
+
+
+def prompt_source_with(prompts: dict, specs_by_id: dict, vocab: int):
+    """Prompt tokens a caller submitted (`EngineCore.submit(spec, prompt_ids)`) take precedence over
+    the seeded synthetic ones."""
+    synth = default_prompt_source(specs_by_id, vocab)
+
+    def src(rid: int) -> np.ndarray:
+        t = prompts.get(rid)
+        return t if t is not None else synth(rid)
+    return src
+
+
+def default_max_rows(requests, num_pages: int) -> int:
+    """Block-table / token-history rows: bounded by concurrency, not by the trace length. A row is
+    bound while its request holds KV (>= 1 page), so `num_pages` rows always suffice for the
+    requests the KV cache can hold; a short trace needs no more rows than it has requests."""
+    return max(1, min(len(requests) or num_pages, num_pages))
+
+
+def default_max_seq_len(requests, floor: int = 16) -> int:
+    """Longest prompt + output of the trace (+1 for the slot of the last sampled token)."""
+    return max([r.input_tokens + r.output_tokens + 1 for r in requests] + [floor])

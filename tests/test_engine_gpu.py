@@ -187,3 +187,58 @@ def test_wall_clock_serving_decision_replay(cuda_ok, lookahead):
         want = plan("throttle", wp, rd, free, pages, ps, 1, [(rid, pq[rid][0], pq[rid][1]) for rid in waiting],
                     [(rid, dq[rid]) for rid in ready], (thr.T, thr.max_p, thr.min_p, thr.kv_thresh, "combined"), 2048)
         assert (dec, chunks) == want[:2], seq
+
+
+def test_metadata_bounds_checks(cuda_ok):
+    """Out-of-range rows / page ids / positions in a micro-batch's metadata are never written through
+    (no block-table or KV write lands outside the stage's tables) and raise at retire."""
+    import ctypes as C
+
+    from paper_2504_14775_b200 import native
+    from paper_2504_14775_b200.errors import NativeError
+    from paper_2504_14775_b200.modelspec import MODELS
+    from paper_2504_14775_b200.stage import PackedBatch, StageWorker
+
+    spec = MODELS["tiny"]
+    w = StageWorker(spec, range(spec.n_layers), is_first=True, is_last=True, num_pages=8, page_size=16, max_rows=4,
+                    max_seq_len=64, max_tokens=64, max_emit=8)
+    native.check_meta_errors()
+    dev = "cuda"
+
+    def prep(info, deltas, prompts=()):
+        hdr, toks = [], []
+        off = 0
+        for row, t in prompts:
+            hdr.append((row, len(t), off))
+            toks += list(t)
+            off += len(t)
+        data = np.array(sum(info, []) + sum([list(d) for d in deltas], []) + sum([list(h) for h in hdr], []) + toks,
+                        np.int32)
+        pb = PackedBatch(0, len(info), sum(i[2] for i in info), 0, 0, 0, len(deltas), len(hdr), data, [], [])
+        md = torch.from_numpy(data).to(dev)
+        T = max(pb.n_tokens, 1)
+        tp, ts, ti, er = (torch.full((T,), -7, dtype=torch.int32, device=dev) for _ in range(4))
+        native.call("gllm_prepare_batch", C.byref(w.cstage), C.byref(w.cbatch(pb, md)), tp.data_ptr(),
+                    ts.data_ptr(), ti.data_ptr(), er.data_ptr(), native.stream_handle())
+        torch.cuda.synchronize()
+        return ts.cpu().tolist()
+
+    table0 = w.block_table.clone()
+    # valid batch: row 1 gets pages 3, 2; tokens 0..19 map to slots on them
+    slots = prep([[1, 0, 20, 0, -1]], [(1, 0, 3), (1, 1, 2)], [(1, list(range(20)))])
+    assert slots == [3 * 16 + p for p in range(16)] + [2 * 16 + p for p in range(4)]
+    assert native.load().gllm_meta_errors(0) == 0
+    before = w.block_table.clone()
+    # bad delta (row 9 of 4, page 99 of 8), bad prompt row, bad seq row, position past max_seq_len
+    prep([[1, 0, 2, 0, -1]], [(9, 0, 1), (1, 2, 99), (1, 40, 1)], [(7, [1, 2])])
+    assert torch.equal(w.block_table, before)             # nothing written through
+    flags = native.load().gllm_meta_errors(0)
+    assert flags & 1 and flags & 2 and not flags & 4, flags
+    with pytest.raises(NativeError):
+        native.check_meta_errors()
+    # a token whose page was never mapped (row 2 is empty) -> slot -1, flagged
+    slots = prep([[2, 0, 3, 0, -1]], [])
+    assert slots == [-1, -1, -1] and native.load().gllm_meta_errors(1) & 8
+    slots = prep([[5, 0, 1, 0, -1], [0, 60, 10, 1, -1]], [])
+    assert slots == [-1] * 11 and native.load().gllm_meta_errors(1) & 4
+    del table0

@@ -82,7 +82,12 @@ def _requests():
     return [RequestSpec(i, float(i) * 0.3, int(rng.integers(5, 60)), int(rng.integers(1, 8))) for i in range(12)]
 
 
-def _run(rank, world, port, q, transport="host"):
+def _prompts():
+    rng = np.random.Generator(np.random.PCG64(99))
+    return {r.id: rng.integers(0, VOCAB, r.input_tokens).astype(np.int32) for r in _requests()}
+
+
+def _run(rank, world, port, q, transport="host", lookahead=False, submit=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2504_14775_b200.pipeline import (HostTransport, MetaChannel, NcclTransport, PipelineExecutor,
@@ -96,11 +101,18 @@ def _run(rank, world, port, q, transport="host"):
     tr = HostTransport(g) if transport == "host" else NcclTransport(rank, make_links(world, backend="gloo"))
     pages = 64
     try:
+        rows = dict(max_rows=len(reqs), max_seq_len=128) if submit else {}
         if rank == 0:
-            ex = PipelineExecutor(SPEC, reqs, world=world, meta=meta, transport=tr, num_pages=pages, page_size=4,
-                                  max_tokens=512, device="cpu", stage_factory=FakeStage)
-            eng = ServingEngine(reqs, pipeline=PipelineConfig(depth=world), kv_config=KvConfig(pages, 4),
-                                throttle=ThrottleConfig(T=2, min_p=4, max_p=64), executor=ex, record_decisions=True)
+            ex = PipelineExecutor(SPEC, [] if submit else reqs, world=world, meta=meta, transport=tr,
+                                  num_pages=pages, page_size=4, max_tokens=512, device="cpu",
+                                  stage_factory=FakeStage, **rows)
+            eng = ServingEngine([] if submit else reqs, pipeline=PipelineConfig(depth=world),
+                                kv_config=KvConfig(pages, 4), throttle=ThrottleConfig(T=2, min_p=4, max_p=64),
+                                executor=ex, record_decisions=True, lookahead=lookahead)
+            if submit:
+                prompts = _prompts()
+                for r in reqs:          # the front end hands requests (and their prompt ids) over
+                    eng.submit(r, prompts[r.id])
             eng.run()
             ex.shutdown()
             raw = eng.raw_data()
@@ -108,8 +120,9 @@ def _run(rank, world, port, q, transport="host"):
                    [(r.id, r.completion_ms is not None) for r in raw.requests], eng.decisions,
                    [(it.prefill_tokens, it.decode_tokens) for it in raw.iterations]))
         else:
-            out = worker_loop(SPEC, reqs, rank=rank, world=world, meta=meta, transport=tr, num_pages=pages,
-                              page_size=4, max_tokens=512, device="cpu", stage_factory=FakeStage)
+            out = worker_loop(SPEC, [] if submit else reqs, rank=rank, world=world, meta=meta, transport=tr,
+                              num_pages=pages, page_size=4, max_tokens=512, device="cpu", stage_factory=FakeStage,
+                              **rows)
             q.put(("worker", rank, out["batches"]))
     except Exception as e:  # surface worker failures to the test
         import traceback
@@ -127,12 +140,17 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,transport", [(2, "host"), (3, "host"), (2, "links"), (3, "links")])
-def test_pipeline_end_to_end_gloo(world, transport):
+@pytest.mark.parametrize("world,transport,lookahead,submit", [
+    (2, "host", False, False), (3, "host", False, False), (2, "links", False, False), (3, "links", False, False),
+    (2, "links", True, False), (3, "links", True, False), (2, "host", True, True)])
+def test_pipeline_end_to_end_gloo(world, transport, lookahead, submit):
+    """`lookahead`: batch b is planned right after batch b-1 launches, with batch b-depth's commit
+    applied (the reference's state at that schedule point); `submit`: requests and their real
+    prompt ids enter through `ServingEngine.submit` instead of the constructor's trace."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, q, transport)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, transport, lookahead, submit)) for r in range(world)]
     for p in procs:
         p.start()
     msgs = [q.get(timeout=120) for _ in range(world)]
@@ -149,10 +167,11 @@ def test_pipeline_end_to_end_gloo(world, transport):
     # tokens: each sampled id is the fake model applied to the previous token at its position,
     # after passing through every stage (all 4 layers) in order
     from paper_2504_14775_b200.workload import prompt_token_ids
+    prompts = _prompts()
     for r in reqs:
         out = outputs[r.id]
         assert len(out) == r.output_tokens
-        hist = list(prompt_token_ids(r.id, r.input_tokens, SPEC.vocab))
+        hist = list(prompts[r.id] if submit else prompt_token_ids(r.id, r.input_tokens, SPEC.vocab))
         for tok in out:
             p = len(hist) - 1
             assert tok == (hist[p] % 251 * 31 + p % 251 + SPEC.n_layers) % VOCAB

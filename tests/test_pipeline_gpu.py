@@ -25,7 +25,7 @@ def _reqs():
     return [RequestSpec(i, float(i) * 2.0, int(rng.integers(20, 200)), int(rng.integers(2, 10))) for i in range(10)]
 
 
-def _run(rank, world, port, q):
+def _run(rank, world, port, q, lookahead=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -42,7 +42,7 @@ def _run(rank, world, port, q):
             ex = PipelineExecutor(spec, reqs, world=world, meta=meta, transport=tr, num_pages=256, page_size=16,
                                   max_tokens=1024, seed=4)
             eng = ServingEngine(reqs, pipeline=PipelineConfig(depth=world), kv_config=KvConfig(256, 16),
-                                throttle=ThrottleConfig(T=4, min_p=16), executor=ex)
+                                throttle=ThrottleConfig(T=4, min_p=16), executor=ex, lookahead=lookahead)
             eng.run()
             ex.shutdown()
             q.put(("ok", {r.id: ex.outputs.get(r.id, []) for r in reqs}))
@@ -58,14 +58,15 @@ def _run(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_pp2_real_stages_share_one_gpu(cuda_ok):
+@pytest.mark.parametrize("lookahead", [False, True])
+def test_pp2_real_stages_share_one_gpu(cuda_ok, lookahead):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_run, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_run, args=(r, 2, port, q, lookahead)) for r in range(2)]
     for p in procs:
         p.start()
     msgs = [q.get(timeout=300) for _ in range(2)]
@@ -96,3 +97,48 @@ def test_pp2_real_stages_share_one_gpu(cuda_ok):
                 clear += 1
                 agree += int(np.argmax(row) == tok)
     assert clear > 0 and agree == clear, (agree, clear)
+
+
+# One command per BASELINE pipeline config (README / DESIGN "Multi-GPU"): bench.py under torchrun,
+# every rank on cuda:0 with host-staged activations (NCCL cannot put two ranks on one GPU).
+# Layers are truncated (--layers) so 8 stage processes fit one GPU; the shapes (d, heads, d_ff,
+# vocab, bias, RoPE scaling), trace, scheduler and depth are the config's own.
+PP_CONFIGS = {
+    "c3_pp2": ["--model", "qwen2.5-14b", "--gpus", "2", "--layers", "8"],
+    "c3_pp4": ["--model", "qwen2.5-14b", "--gpus", "4", "--layers", "8"],
+    "c4_pp4_throttle": ["--model", "qwen2.5-32b", "--gpus", "4", "--layers", "8", "--scheduler", "throttle"],
+    "c4_pp4_sarathi": ["--model", "qwen2.5-32b", "--gpus", "4", "--layers", "8", "--scheduler", "sarathi"],
+    "c5_pp8": ["--model", "llama3.1-70b", "--gpus", "8", "--layers", "8", "--trace", "c5", "--rate", "4"],
+}
+
+
+@pytest.mark.parametrize("name", list(PP_CONFIGS))
+def test_bench_pipeline_configs_one_gpu(cuda_ok, name):
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = PP_CONFIGS[name]
+    n = args[args.index("--gpus") + 1]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", "bench.py", *args,
+           "--n-requests", "48", "--steps", "4", "--warmup", "3", "--warm-max-iters", "6", "--profile-steps", "3",
+           "--no-cpu-baseline"]
+    env = dict(os.environ, GLLM_PP_TRANSPORT="host")
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    print(f"\n{name}: {line['value']:.1f} tok/s device window, e2e {line['e2e']['value']:.1f}, "
+          f"bubble {line['serving']['bubble_frac_per_stage']}, dominant {line['roofline']['kernel']}")
+    assert line["n_gpus"] == int(n) and line["config"]["parallelism"] == f"pp{n}"
+    assert line["steps"] == 4 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert len(line["serving"]["bubble_frac_per_stage"]) == int(n)
+    assert all(0.0 <= b <= 1.0 for b in line["serving"]["bubble_frac_per_stage"])
+    # the profiled window covers every stage: the last stage's LM head and the first's embedding
+    assert "gemm_lm_head" in line["roofline"]["classes"] and "embed" in line["roofline"]["classes"]
+    assert line["gpu_launches"] > 0
