@@ -403,9 +403,12 @@ def run_ours(args, dd: _Dist):
             st["count"] += 1
             if st["count"] >= W:
                 # timed region starts here. With lookahead the batches already launched are not
-                # timed: only batches launched after t0 count (their seq > the last launched one).
+                # timed: only batches launched after t0 count (their seq > the last launched one);
+                # on PP>1 the sync covers rank 0's GPU only -- later stages may still hold older batches,
+                # which is the pipeline's steady state.
                 st["phase"] = "timed"
                 st["first_seq"] = max([s for s, _ in eng.launch_log], default=seq) + 1
+                torch.cuda.synchronize()          # drain the already-queued (untimed) batch
                 st["timed_start"] = time.perf_counter()
                 st["launch0"] = native.launch_count()
                 torch.cuda.nvtx.range_push("bench_timed")   # ncu --nvtx --nvtx-include bench_timed/

@@ -135,7 +135,7 @@ class LocalExecutor:
             logits_host = None
             if self.record_logits and pb.n_emit:
                 logits_host = self.logits_dev[:pb.n_emit].to("cpu", non_blocking=True)
-            done = torch.cuda.Event()
+            done = torch.cuda.Event(enable_timing=True)
             done.record(st)
         self.ring.fence(k, done)
         self._inflight[pb.seq] = (pb, done, host, logits_host)

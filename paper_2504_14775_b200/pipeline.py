@@ -245,8 +245,7 @@ class PipelineExecutor:
         # receive from the last rank (different peers, independent progress)
         self.send_stream = torch.cuda.Stream(device=self.device) if on_gpu else None
         self.recv_stream = torch.cuda.Stream(device=self.device) if on_gpu else None
-        if ring < world + 2:
-            raise ValueError(f"ring={ring} must be >= world + 2 (batches in flight + one queued)")
+        ring = max(ring, world + 2)    # depth batches in flight + one queued + one being packed
         self.ring = ring
         self.lag = lag if lag is not None else world
         n_ints = 16 * max_tokens + 8 * max_rows + 4 * max_seq_len
@@ -421,6 +420,7 @@ def worker_loop(spec: ModelSpec, requests, *, rank: int, world: int, meta: MetaC
                         num_pages=num_pages, page_size=page_size, max_rows=max_rows, max_seq_len=max_seq_len,
                         max_tokens=max_tokens, max_emit=max_emit, seed=seed, device=dev)
     on_gpu = dev.type == "cuda"
+    ring = max(ring, world + 2)
     compute = torch.cuda.Stream(device=dev) if on_gpu else None
     recv_s = torch.cuda.Stream(device=dev) if on_gpu else None
     send_s = torch.cuda.Stream(device=dev) if on_gpu else None

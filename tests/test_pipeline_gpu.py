@@ -131,7 +131,8 @@ def test_bench_pipeline_configs_one_gpu(cuda_ok, name):
            "--no-cpu-baseline"]
     env = dict(os.environ, GLLM_PP_TRANSPORT="host")
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    rank0 = "\n".join(ln for ln in r.stderr.splitlines() if "[rank0]" in ln or "Error" in ln)
+    assert r.returncode == 0, r.stdout[-2000:] + rank0[-6000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     print(f"\n{name}: {line['value']:.1f} tok/s device window, e2e {line['e2e']['value']:.1f}, "
           f"bubble {line['serving']['bubble_frac_per_stage']}, dominant {line['roofline']['kernel']}")
