@@ -33,7 +33,7 @@ from bisect import bisect_left, insort
 from dataclasses import dataclass, field
 
 from .errors import ConfigError, UnschedulableError
-from .kvcache import KvCacheState, KvConfig, PagedKvCache, pages_needed
+from .kvcache import KvCacheState, KvConfig, PagedKvCache, PrefixCachingKvCache, pages_needed, prompt_page_hashes
 from .metrics import IterationRecord, RequestRecord
 from .sched import MicroBatchPlan, ThrottleConfig, fill_prefill, prefill_token_limit, throttle_decode
 from .workload import RequestSpec
@@ -199,6 +199,7 @@ class _Batch:
     stage_ms: float
     transfer_ms: float
     meta: BatchMeta | None = None
+    stage_list: list[float] | None = None   # per-stage measured device ms (measured-time replay)
 
 
 @dataclass
@@ -224,7 +225,7 @@ class EngineCore:
     def __init__(self, requests: list[RequestSpec], scheduler: str = "throttle",
                  pipeline: PipelineConfig | None = None, kv_config: KvConfig | None = None,
                  throttle: ThrottleConfig | None = None, token_budget: int = 2048,
-                 executor=None, max_rows: int | None = None):
+                 executor=None, max_rows: int | None = None, prefix_caching: bool = False):
         if scheduler not in SCHEDULERS:
             raise ConfigError(f"scheduler must be one of {SCHEDULERS}, got {scheduler!r}")
         self._scheduler = scheduler
@@ -251,7 +252,14 @@ class EngineCore:
         self._reqs: dict[int, _Req] = {s.id: _Req(s) for s in requests}
         self._order = [s.id for s in requests]
         self.executor = executor
-        self.kv: KvCacheState = PagedKvCache(kv_config) if executor is not None else KvCacheState(kv_config)
+        if prefix_caching and (executor is None or not hasattr(executor, "prompt_source")):
+            raise ConfigError("prefix caching needs a GPU executor with prompt tokens")
+        # Prefix caching (opt-in; the reference has none): full prompt pages shared by requests
+        # with equal token prefixes, see `_match_prefixes` and `PrefixCachingKvCache`.
+        self._prefix = prefix_caching
+        self._hashes: dict[int, list[int]] = {}
+        self.kv: KvCacheState = (PrefixCachingKvCache(kv_config) if prefix_caching else
+                                 PagedKvCache(kv_config) if executor is not None else KvCacheState(kv_config))
         self._rows_free: list[int] = []
         self._rows_next = 0
         if max_rows is None:
@@ -398,6 +406,8 @@ class EngineCore:
             r.inflight = 0
             r.done += n
             r.incarnation += n
+            if self._prefix:
+                self.kv.register(rid, self._page_hashes(rid), min(r.done, r.spec.input_tokens))
             if r.done >= r.target:
                 self._enter_decode(r)
                 if r.generated == 0:
@@ -507,11 +517,47 @@ class EngineCore:
                 raise AssertionError("prefill pages were reserved at planning time")
         return mutated
 
+    def _page_hashes(self, rid: int) -> list[int]:
+        h = self._hashes.get(rid)
+        if h is None:
+            h = prompt_page_hashes(self.executor.prompt_source(rid), self.kv.config.page_size)
+            self._hashes[rid] = h
+        return h
+
+    def _match_prefixes(self) -> None:
+        """Prefix caching: before planning, requests at the head of the FCFS queue that hold no KV
+        map the registered pages of their prompt prefix (at least one prompt token is always left
+        to compute, it yields the first token); their prefill starts after the cached tokens, so
+        #WP drops by them. Only the head that the next prefill budget can reach is examined."""
+        kv = self.kv
+        ps = kv.config.page_size
+        budget = self._throttle.max_p if self._scheduler == "throttle" else self._token_budget
+        seen = 0
+        for _, rid in list(self._waiting):
+            r = self._reqs[rid]
+            if r.done == 0 and not r.in_flight and kv.stored_tokens(rid) == 0:
+                hashes = self._page_hashes(rid)
+                limit = min(len(hashes), (r.target - 1) // ps)
+                if limit > 0:
+                    if r.row < 0:
+                        if not self._rows_free and self._rows_next >= self._max_rows:
+                            break
+                        self._bind_row(rid)
+                    got = kv.match(rid, hashes, limit)
+                    if got:
+                        r.done = got      # cached, not computed: no incarnation (discard) credit
+                        self._wp -= got
+            seen += r.target - r.done
+            if seen >= budget:
+                break
+
     def _try_plan(self) -> MicroBatchPlan | None:
         """Plan + allocate; re-plan after an eviction that emptied the plan (`engine.py:391-408`)."""
         while True:
             if not self._waiting and not self._ready:
                 return None
+            if self._prefix:
+                self._match_prefixes()
             plan = self._plan()
             mutated = self._apply_kv(plan)
             if not plan.is_empty():
@@ -609,11 +655,22 @@ class Engine(EngineCore):
                  pipeline: PipelineConfig | None = None, kv_config: KvConfig | None = None,
                  throttle: ThrottleConfig | None = None, token_budget: int = 2048,
                  horizon_ms: float | None = None, record_events: bool = False,
-                 executor=None, max_rows: int | None = None):
+                 executor=None, max_rows: int | None = None, measured_stage_times: bool = False,
+                 prefix_caching: bool = False):
         super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget,
-                         executor, max_rows)
+                         executor, max_rows, prefix_caching)
         if horizon_ms is not None and horizon_ms < 0:
             raise ConfigError(f"horizon_ms must be >= 0, got {horizon_ms}")
+        if measured_stage_times:
+            n = len(getattr(executor, "stages", ()))
+            if executor is None or not hasattr(executor, "stage_times_ms") or n != self._pipeline.depth:
+                raise ConfigError("measured_stage_times needs an executor holding pipeline.depth stages "
+                                  "with stage_times_ms(seq)")
+        # Measured-time replay: each stage's duration is that stage's measured device time for this
+        # micro-batch (all stages executed for real, one at a time on one GPU, CUDA-event timed)
+        # instead of `stage_time`'s cost model; the event loop (in-order admission, transfers,
+        # commit order, the schedule gate) is unchanged.
+        self._measured = measured_stage_times
         self._horizon = horizon_ms
         self._events = [] if record_events else None
         depth = self._pipeline.depth
@@ -683,7 +740,8 @@ class Engine(EngineCore):
         while self._expect[stage] in pend:
             seq = self._expect[stage]
             start = max(pend.pop(seq), self._free_at[stage])
-            end = start + self.in_flight[seq].stage_ms
+            b = self.in_flight[seq]
+            end = start + (b.stage_list[stage] if b.stage_list is not None else b.stage_ms)
             self._busy[stage].append((start, end))
             self._spans.append((seq, stage, start, end))
             self._free_at[stage] = end
@@ -700,7 +758,9 @@ class Engine(EngineCore):
         self._log(t, SCHEDULE_POINT, 0, batch.seq, plan)
         if self.executor is not None:
             self.executor.launch(batch.meta)
-        end = t + batch.stage_ms
+            if self._measured:
+                batch.stage_list = self.executor.stage_times_ms(batch.seq)
+        end = t + (batch.stage_list[0] if batch.stage_list is not None else batch.stage_ms)
         self._busy[0].append((t, end))
         self._spans.append((batch.seq, 0, t, end))
         self._free_at[0] = end

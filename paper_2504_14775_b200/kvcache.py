@@ -205,3 +205,134 @@ def select_preemption_victim(candidates: Iterable[tuple[int, float]]) -> int | N
         if best is None or (arrival, rid) > best:
             best = (arrival, rid)
     return None if best is None else best[1]
+
+
+def prompt_page_hashes(tokens, page_size: int) -> list[int]:
+    """Chained hashes of the full pages of a prompt: h_i = H(h_{i-1}, tokens of page i). Equal
+    hashes mean equal token prefixes (up to 64-bit collisions), so page i's KV can be shared."""
+    import hashlib
+
+    t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
+    out, prev = [], b""
+    for i in range(len(t) // page_size):
+        d = hashlib.blake2b(prev + t[i * page_size:(i + 1) * page_size].tobytes(), digest_size=8).digest()
+        out.append(int.from_bytes(d, "little"))
+        prev = d
+    return out
+
+
+class PrefixCachingKvCache(PagedKvCache):
+    """PagedKvCache whose full prompt pages are shared between requests with the same token prefix
+    (the paper's prefix caching, `PAPER.md:325`; absent from the reference's cost model).
+
+    * Every physical page has a reference count. A prompt page whose KV is complete is registered
+      under its chained prefix hash (`register`); a later request whose prompt starts with the
+      same pages maps them into its block-table row (`match`) instead of recomputing them.
+    * A page whose last holder releases it stays cached while its hash is registered: it counts
+      as free for the scheduler (Token Throttling sees the same free/total ratio as without
+      sharing) and is reclaimed least-recently-released first when the free stack runs dry.
+    * Counts keep the reference's meaning per request: `stored_tokens` / `pages` include shared
+      pages; `free_pages` counts each physical page once.
+    """
+
+    def __init__(self, config: KvConfig):
+        super().__init__(config)
+        from collections import OrderedDict
+
+        self._ref: dict[int, int] = {}
+        self._by_hash: dict[int, int] = {}
+        self._hash_of: dict[int, int] = {}
+        self._cached: "OrderedDict[int, None]" = OrderedDict()   # ref 0, hash registered: reclaimable
+        self.hit_tokens = 0
+
+    def _take_page(self) -> int:
+        if self._stack:
+            return self._stack.pop()
+        pid, _ = self._cached.popitem(last=False)      # least recently released cached page
+        del self._by_hash[self._hash_of.pop(pid)]
+        return pid
+
+    def _grant(self, request_id: int, n_pages: int) -> None:
+        owned = self._owned.setdefault(request_id, [])
+        row = self._row.get(request_id, -1)
+        if row < 0:
+            raise ConfigError(f"request {request_id} has no block-table row")
+        base = len(owned)
+        for k in range(n_pages):
+            pid = self._take_page()
+            self._ref[pid] = 1
+            owned.append(pid)
+            self._delta_row.append(row)
+            self._delta_idx.append(base + k)
+            self._delta_page.append(pid)
+
+    def _revoke(self, request_id: int) -> None:
+        owned = self._owned.pop(request_id, [])
+        freed = []
+        for pid in owned:
+            r = self._ref[pid] - 1
+            if r:
+                self._ref[pid] = r
+                continue
+            del self._ref[pid]
+            if pid in self._hash_of:
+                self._cached[pid] = None
+            else:
+                freed.append(pid)
+        self._stack.extend(reversed(freed))
+
+    def release(self, request_id: int) -> int:
+        """Release every page the request maps; `free_pages` grows by the pages no one else holds."""
+        if request_id not in self._pages:
+            raise KeyError(f"request {request_id} holds no pages")
+        before = len(self._stack) + len(self._cached)
+        n = self._pages.pop(request_id)
+        del self._tokens[request_id]
+        self._revoke(request_id)
+        self.free_pages += len(self._stack) + len(self._cached) - before
+        return n
+
+    def match(self, request_id: int, hashes: list[int], max_pages: int) -> int:
+        """Map the longest registered prefix (<= max_pages pages) of `hashes` into this request's
+        row, which must hold no KV yet. Returns the tokens now cached (pages x page_size)."""
+        if self._tokens.get(request_id, 0):
+            raise ConfigError(f"request {request_id} already holds KV")
+        row = self._row.get(request_id, -1)
+        if row < 0:
+            raise ConfigError(f"request {request_id} has no block-table row")
+        pids = []
+        for h in hashes[:max_pages]:
+            pid = self._by_hash.get(h)
+            if pid is None:
+                break
+            pids.append(pid)
+        if not pids:
+            return 0
+        owned = self._owned.setdefault(request_id, [])
+        for k, pid in enumerate(pids):
+            if pid in self._cached:
+                del self._cached[pid]
+                self.free_pages -= 1
+                self._ref[pid] = 1
+            else:
+                self._ref[pid] += 1
+            owned.append(pid)
+            self._delta_row.append(row)
+            self._delta_idx.append(k)
+            self._delta_page.append(pid)
+        n_tok = len(pids) * self.config.page_size
+        self._tokens[request_id] = n_tok
+        self._pages[request_id] = len(pids)
+        self.hit_tokens += n_tok
+        return n_tok
+
+    def register(self, request_id: int, hashes: list[int], n_tokens: int) -> None:
+        """The request's first `n_tokens` prompt tokens have their KV written: publish the full
+        pages among them under their prefix hashes (first writer wins)."""
+        owned = self._owned.get(request_id, ())
+        for i in range(min(n_tokens // self.config.page_size, len(hashes), len(owned))):
+            h, pid = hashes[i], owned[i]
+            if h in self._by_hash or pid in self._hash_of:
+                continue
+            self._by_hash[h] = pid
+            self._hash_of[pid] = h

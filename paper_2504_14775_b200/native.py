@@ -131,15 +131,27 @@ def stream_handle(stream=None) -> int:
     return s.cuda_stream
 
 
+_profiling = False
+
+
 def profile_begin() -> None:
+    global _profiling
     call("gllm_profile_begin")
+    _profiling = True
+
+
+def profiling() -> bool:
+    """The native per-launch profiler is on (its CUDA events cannot live inside a captured graph)."""
+    return _profiling
 
 
 def profile_end() -> dict[str, dict]:
     """Aggregated per-kernel-class CUDA-event timings captured since `profile_begin`."""
+    global _profiling
     arr = (ProfileEntry * 64)()
     n = C.c_int(0)
     call("gllm_profile_end", arr, 64, C.byref(n))
+    _profiling = False
     return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
                                    "flops": arr[i].flops, "bytes": arr[i].bytes} for i in range(n.value)}
 

@@ -32,10 +32,12 @@ class ServingEngine(EngineCore):
     def __init__(self, requests, scheduler: str = "throttle", pipeline: PipelineConfig | None = None,
                  kv_config: KvConfig | None = None, throttle: ThrottleConfig | None = None,
                  token_budget: int = 2048, executor=None, max_rows: int | None = None,
-                 time_scale: float = 1.0, record_decisions: bool = False, lookahead: bool = False):
+                 time_scale: float = 1.0, record_decisions: bool = False, lookahead: bool = False,
+                 prefix_caching: bool = False):
         if executor is None:
             raise ValueError("ServingEngine needs a GPU executor")
-        super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget, executor, max_rows)
+        super().__init__(requests, scheduler, pipeline, kv_config, throttle, token_budget, executor, max_rows,
+                         prefix_caching)
         self._arrivals = sorted(requests, key=lambda s: (s.arrival_ms, s.id))
         self._arrival_keys = [(s.arrival_ms, s.id) for s in self._arrivals]
         self._next_arrival = 0

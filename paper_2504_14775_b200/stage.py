@@ -93,7 +93,9 @@ class StageWorker:
 
     def __init__(self, spec: ModelSpec, layers: range, *, is_first: bool, is_last: bool, num_pages: int,
                  page_size: int, max_rows: int, max_seq_len: int, max_tokens: int, max_emit: int,
-                 seed: int = 0, device="cuda", fused_norm: bool | None = None):
+                 seed: int = 0, device="cuda", fused_norm: bool | None = None, scratch: bool = False):
+        """`scratch`: one extra block-table row and KV page past the engine's (max_rows, num_pages),
+        the target of the padding sequences of CUDA-graph decode batches (`executor.LocalExecutor`)."""
         import torch
 
         lib = native.load()
@@ -122,12 +124,18 @@ class StageWorker:
         self.final_norm = init_embed(spec, seed, dev, "final_norm") if is_last else None
         self.lm_head = init_embed(spec, seed, dev, "lm_head") if is_last else None
         L = len(self.layer_ids)
+        self.scratch_row = max_rows if scratch else None
+        self.scratch_page = num_pages if scratch else None
+        if scratch:
+            max_rows, num_pages = max_rows + 1, num_pages + 1
         kv_shape = (L, num_pages, spec.n_kv_heads, page_size, spec.head_dim)
         self.k_cache = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
         self.v_cache = torch.empty(kv_shape, dtype=torch.bfloat16, device=dev)
         self.max_pages_per_row = -(-max_seq_len // page_size)
         # -1 = unmapped: a position whose page was never delivered fails the device bounds check
         self.block_table = torch.full((max_rows, self.max_pages_per_row), -1, dtype=torch.int32, device=dev)
+        if scratch:
+            self.block_table[self.scratch_row, 0] = self.scratch_page
         self.token_hist = torch.zeros((max_rows, max_seq_len), dtype=torch.int32, device=dev) if is_first else None
         self.rope = torch.from_numpy(rope_table(spec, max_seq_len)).to(dev)
         self.dims = native.Dims(L, spec.d_model, spec.n_heads, spec.n_kv_heads, spec.head_dim, spec.d_ff, spec.vocab,
@@ -182,6 +190,26 @@ class StageWorker:
         b = self.cbatch(pb, meta_dev)
         native.call("gllm_commit_tokens", C.byref(self.cstage), C.byref(b), native.ptr(sampled),
                     native.stream_handle(stream))
+
+
+def pad_decode_batch(pb: PackedBatch, bucket: int, scratch_row: int, scratch_page: int) -> PackedBatch:
+    """A decode-only batch padded to `bucket` sequences for a captured CUDA graph: the padding
+    sequences decode token 0 of the scratch row (its one KV page is the scratch page) and the
+    block-table deltas are padded with the scratch row's own (idempotent) entry, so every count
+    the device sees is fixed per bucket. Sampled rows past pb.n_emit are ignored by the caller."""
+    n, nd = pb.n_seqs, pb.n_deltas
+    d = pb.data
+    info = d[:5 * n].reshape(n, 5)
+    work = d[5 * n:7 * n].reshape(n, 2)
+    deltas = d[7 * n:7 * n + 3 * nd].reshape(nd, 3)
+    pad = bucket - n
+    j = np.arange(n, bucket, dtype=np.int32)
+    pinfo = np.stack([np.full(pad, scratch_row, np.int32), np.zeros(pad, np.int32), np.ones(pad, np.int32), j, j], axis=1)
+    pwork = np.stack([j, np.zeros(pad, np.int32)], axis=1)
+    pdel = np.tile(np.asarray([[scratch_row, 0, scratch_page]], np.int32), (bucket - nd, 1))
+    data = np.concatenate([info.ravel(), pinfo.ravel(), work.ravel(), pwork.ravel(), deltas.ravel(),
+                           pdel.ravel()]).astype(np.int32)
+    return PackedBatch(pb.seq, bucket, bucket, bucket, bucket, 0, bucket, 0, data, pb.emit_ids, pb.emit_pos, pb.flags)
 
 
 def default_prompt_source(specs_by_id: dict, vocab: int):

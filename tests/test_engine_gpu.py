@@ -242,3 +242,84 @@ def test_metadata_bounds_checks(cuda_ok):
     slots = prep([[5, 0, 1, 0, -1], [0, 60, 10, 1, -1]], [])
     assert slots == [-1] * 11 and native.load().gllm_meta_errors(1) & 4
     del table0
+
+
+@pytest.mark.parametrize("n_stages", [1, 2])
+def test_cuda_graph_decode_batches(cuda_ok, n_stages):
+    """Decode-only micro-batches replayed from captured CUDA graphs (padded batch buckets): the
+    virtual-clock schedule is unchanged, every request completes, and the sampled-step logits stay
+    within 2e-2 of the fp32 oracle with tokens equal to its argmax wherever the margin is clear."""
+    from oracle.model_ref import from_stage_workers
+    from paper_2504_14775_b200.executor import LocalExecutor
+    from paper_2504_14775_b200.modelspec import MODELS
+
+    spec = MODELS["tiny"]
+    reqs = _c1()
+    watch = [0, 5, 17, 40]
+    ex = LocalExecutor(spec, reqs, num_pages=4096, page_size=16, n_stages=n_stages, max_tokens=2560,
+                       record_logits=True, record_ids=watch, seed=1, cuda_graphs=True)
+    eng = Engine(reqs, scheduler="throttle", pipeline=PipelineConfig(depth=1), kv_config=KvConfig(4096, 16),
+                 throttle=ThrottleConfig(), executor=ex)
+    raw = eng.run()
+    gold = {r["name"]: r for r in ENGINE["runs"]}["c1_throttle_d1"]
+    assert [[it.batch_seq, it.schedule_time_ms, it.prefill_tokens, it.decode_tokens] for it in raw.iterations] \
+        == gold["iterations"]
+    assert ex.graph_replays > 20 and len(ex._graphs) >= 2, (ex.graph_replays, list(ex._graphs))
+    for r in reqs:
+        assert len(ex.outputs[r.id]) == r.output_tokens
+    oracle = from_stage_workers(ex.stages)
+    by_req = {}
+    for rid, pos, lg in ex.logits:
+        by_req.setdefault(rid, []).append((pos, lg))
+    worst, agree, clear = 0.0, 0, 0
+    for rid in watch:
+        spec_r = reqs[rid]
+        seq = np.concatenate([prompt_token_ids(rid, spec_r.input_tokens, spec.vocab),
+                              np.asarray(ex.outputs[rid][:-1], dtype=np.int32)])
+        ref = oracle.logits(seq).numpy()
+        for pos, lg in by_req[rid]:
+            want = ref[pos - 1]
+            worst = max(worst, np.linalg.norm(lg - want) / np.linalg.norm(want))
+            top2 = np.sort(want)[-2:]
+            if top2[1] - top2[0] > 0.05:
+                clear += 1
+                agree += int(np.argmax(lg) == np.argmax(want))
+    print(f"cuda graphs, {n_stages} stage(s): {ex.graph_replays} replays over {len(ex._graphs)} graphs, "
+          f"worst logits rel err {worst:.3e}")
+    assert worst < 2e-2, worst
+    assert clear > 0 and agree == clear, (agree, clear)
+
+
+def test_prefix_caching_logits(cuda_ok):
+    """Requests sharing a 6-page system prompt: later requests map the cached pages instead of
+    recomputing them; their sampled-step logits still match the fp32 oracle run on the FULL
+    prompt (so the shared KV pages hold exactly the prefix's keys and values)."""
+    from oracle.model_ref import from_stage_workers
+    from paper_2504_14775_b200.executor import LocalExecutor
+    from paper_2504_14775_b200.modelspec import MODELS
+
+    spec = MODELS["tiny"]
+    rng = np.random.default_rng(5)
+    system = rng.integers(0, spec.vocab, 96).astype(np.int32)
+    reqs, prompts = [], {}
+    for i in range(10):
+        tail = rng.integers(0, spec.vocab, int(rng.integers(3, 50))).astype(np.int32)
+        prompts[i] = np.concatenate([system, tail])
+        reqs.append(RequestSpec(i, 4.0 * i, len(prompts[i]), 5))
+    ex = LocalExecutor(spec, reqs, num_pages=512, page_size=16, max_tokens=1024, record_logits=True, seed=2)
+    for i, p in prompts.items():
+        ex.register_prompt(i, p)
+    eng = Engine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(512, 16), executor=ex,
+                 throttle=ThrottleConfig(T=2, min_p=8), prefix_caching=True)
+    eng.run()
+    assert eng.kv.hit_tokens >= 8 * 96, eng.kv.hit_tokens
+    oracle = from_stage_workers(ex.stages)
+    worst = 0.0
+    for rid, pos, lg in ex.logits:
+        seq = np.concatenate([prompts[rid], np.asarray(ex.outputs[rid], dtype=np.int32)])[:pos]
+        want = oracle.logits(seq).numpy()[pos - 1]
+        worst = max(worst, float(np.linalg.norm(lg - want) / np.linalg.norm(want)))
+    for r in reqs:
+        assert len(ex.outputs[r.id]) == r.output_tokens
+    print(f"prefix caching: {eng.kv.hit_tokens} cached prompt tokens reused, worst logits rel err {worst:.3e}")
+    assert worst < 2e-2, worst

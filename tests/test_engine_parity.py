@@ -155,3 +155,64 @@ def test_scale_runs(case):
         (case["makespan"], case["preemptions"], case["committed"], case["discarded"])
     rep = build_report(raw)
     assert (rep.token_stddev, rep.bubble_mean) == (case["token_stddev"], case["bubble_mean"])
+
+
+class _TimedFakeExecutor:
+    """Executor stand-in for the measured-time replay: reports per-stage 'device' times."""
+
+    def __init__(self, depth, times_fn):
+        self.stages = [object()] * depth
+        self.max_rows = None
+        self.times_fn = times_fn
+        self.plans = {}
+
+    def launch(self, meta):
+        self.plans[meta.seq] = meta
+
+    def stage_times_ms(self, seq):
+        return self.times_fn(self.plans[seq])
+
+    def retire(self, seq):
+        pass
+
+    def on_finish(self, request_id, row):
+        pass
+
+
+@pytest.mark.parametrize("depth", [1, 2, 4])
+def test_measured_stage_times_reduce_to_cost_model(depth):
+    """Replay with per-stage times equal to `stage_time` reproduces the cost-model timeline exactly."""
+    from paper_2504_14775_b200.engine import stage_time
+    reqs = _specs(TRACES[ENGINE["runs"][0]["trace"]])
+    cost = StageCostModel(1.0, 0.01, 0.1)
+    pipe = PipelineConfig(depth=depth, cost=cost)
+    kv = KvConfig(2048, 16)
+    ref = run(reqs, pipeline=pipe, kv_config=kv)
+
+    eng = None
+
+    def times(meta):
+        plan = eng.in_flight[meta.seq].plan
+        return [stage_time(plan, cost)] * depth
+
+    eng = Engine(reqs, pipeline=pipe, kv_config=kv, executor=_TimedFakeExecutor(depth, times),
+                 measured_stage_times=True)
+    got = eng.run()
+    assert _timeline(got) == _timeline(ref)
+
+
+def test_measured_stage_times_per_stage():
+    """Unequal per-stage times: each stage span lasts exactly its measured time, admission stays in order."""
+    reqs = _specs(TRACES[ENGINE["runs"][0]["trace"]])[:20]
+    per_stage = [0.7, 2.5, 1.1]
+    eng = Engine(reqs, pipeline=PipelineConfig(depth=3), kv_config=KvConfig(2048, 16),
+                 executor=_TimedFakeExecutor(3, lambda m: list(per_stage)), measured_stage_times=True)
+    raw = eng.run()
+    assert all(r.finished for r in raw.requests)
+    for seq, stage, a, b in raw.stage_spans:
+        assert b - a == pytest.approx(per_stage[stage])
+    for ivs in raw.busy_intervals:
+        assert all(ivs[i][1] <= ivs[i + 1][0] for i in range(len(ivs) - 1))
+    with pytest.raises(Exception):
+        Engine(reqs, pipeline=PipelineConfig(depth=2), executor=_TimedFakeExecutor(3, lambda m: per_stage),
+               measured_stage_times=True)

@@ -64,3 +64,21 @@ def test_pack_batch_layout():
     assert d[25:31].tolist() == [5, 0, 11, 5, 1, 12]
     assert d[31:34].tolist() == [5, 3, 0] and d[34:].tolist() == [100, 101, 102]
     assert pb.emit_ids == [7, 4] and pb.emit_pos == [41, 15]
+
+
+def test_pad_decode_batch_layout():
+    """CUDA-graph padding: real decodes keep their entries, padding sequences decode the scratch row."""
+    import numpy as np
+
+    from paper_2504_14775_b200.engine import BatchMeta, SeqMeta
+    from paper_2504_14775_b200.stage import pack_batch, pad_decode_batch
+    meta = BatchMeta.from_seqs(8, [SeqMeta(7, 2, 40, 1, True), SeqMeta(4, 1, 31, 1, True)],
+                               np.array([[1, 2, 33]], np.int32), [])
+    pb = pack_batch(meta, 32, lambda rid: None)
+    pp = pad_decode_batch(pb, 4, scratch_row=50, scratch_page=900)
+    assert (pp.n_seqs, pp.n_tokens, pp.n_emit, pp.n_work, pp.n_prefill_work, pp.n_deltas, pp.n_prompts) == (4, 4, 4, 4, 0, 4, 0)
+    d = pp.data
+    assert d[:20].tolist() == [2, 40, 1, 0, 0, 1, 31, 1, 1, 1, 50, 0, 1, 2, 2, 50, 0, 1, 3, 3]
+    assert d[20:28].tolist() == [0, 0, 1, 0, 2, 0, 3, 0]
+    assert d[28:40].tolist() == [1, 2, 33, 50, 0, 900, 50, 0, 900, 50, 0, 900]
+    assert d.size == 40 and pp.emit_ids == [7, 4] and pp.seq == 8

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--batch", type=int, default=4)
     ap.add_argument("--ctx", type=int, default=512)
     ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--cuda-graphs", action="store_true", help="decode-only batches as captured CUDA graphs")
     a = ap.parse_args()
 
     import torch
@@ -43,7 +44,8 @@ def main():
     pf_iters = -(-a.batch * a.ctx // 2048) + 8
     reqs = [RequestSpec(i, 0.0, a.ctx, warm + a.steps + 8 + pf_iters) for i in range(a.batch)]
     pages = a.batch * (-(-(a.ctx + warm + a.steps + 16 + pf_iters) // 16)) + 64
-    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, max_tokens=2048, max_emit=max(a.batch, 32), seed=0)
+    ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, max_tokens=2048, max_emit=max(a.batch, 32), seed=0,
+                       cuda_graphs=a.cuda_graphs)
     eng = Engine(reqs, pipeline=PipelineConfig(depth=1), kv_config=KvConfig(pages, 16), throttle=ThrottleConfig(),
                  executor=ex)
     decode_only, ranged, wall = [], False, []
@@ -77,7 +79,8 @@ def main():
     # host wall time per decode step through the engine (planning, packing, launches, token read-back)
     gaps = [b - a_ for a_, b in zip(wall[warm // 2:], wall[warm // 2 + 1:])]
     wall_ms = statistics.median(gaps) * 1e3 if gaps else None
-    print(json.dumps({"model": a.model, "batch": a.batch, "ctx": a.ctx, "steps": len(ms), "ms_per_step": round(med, 3),
+    print(json.dumps({"model": a.model, "batch": a.batch, "ctx": a.ctx, "cuda_graphs": a.cuda_graphs,
+                      "graph_replays": ex.graph_replays, "steps": len(ms), "ms_per_step": round(med, 3),
                       "wall_ms_per_step": round(wall_ms, 3) if wall_ms else None,
                       "weight_floor_ms": round(floor_ms, 3), "frac_of_floor": round(floor_ms / med, 3)}))
 
