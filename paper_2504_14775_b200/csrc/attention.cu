@@ -17,15 +17,18 @@
 //    the G heads sharing the kv head), attended against the cached prefix plus
 //    the chunk's own earlier tokens in 128-key blocks, FlashAttention-style and
 //    warp-specialised: warp 8 streams K/V blocks from the paged cache with 2-D
-//    TMA (one box per page and 64-dim half, 128B-swizzled) into a 5-slot ring;
-//    warp 9 issues every tcgen05.mma (S = Q.K^T with Q, K from smem; O += P.V
-//    with P read straight from TMEM, V as an MN-major smem operand); warps 0-3
-//    and 4-7 run the online softmax of query tile 0 and 1, one thread per TMEM
-//    lane (= query row). The two tiles ping-pong: while one tile's softmax runs
-//    on the CUDA cores the tensor core computes the other tile's P.V and next
-//    S. S/P (aliased, P as packed bf16 over S's first 64 columns) and O take
-//    all 512 TMEM columns; O is rescaled in TMEM only when a row's max grows by
-//    more than 8 (log2 units), the exact "lazy rescale" form of online softmax.
+//    TMA (one box per page and 64-dim half, 128B-swizzled) into a 5-slot ring, one
+//    lane per page with the page ids read a block ahead; warp 9 issues every
+//    tcgen05.mma (S = Q.K^T with Q, K from smem; O += P.V with P read straight from
+//    TMEM, V as an MN-major smem operand); warps 0-3 and 4-7 run the online softmax
+//    of query tile 0 and 1, one thread per TMEM lane (= query row), with the row's
+//    128 scores in registers (one TMEM read, 3-input max, MUFU exp2): setmaxnreg
+//    moves registers from the producer warpgroup (warps 8-11) to the softmax ones.
+//    The two tiles ping-pong: while one tile's softmax runs on the CUDA cores the
+//    tensor core computes the other tile's P.V and next S. S/P (aliased, P as packed
+//    bf16 over S's first 64 columns) and O take all 512 TMEM columns; O is rescaled
+//    in TMEM only when a row's max grows by more than 8 (log2 units), the exact
+//    "lazy rescale" form of online softmax.
 //
 // Cache layout [page][kv_head][slot][hd] (stage.py); pages resolved through the
 // device block table. Work list: int32 (seq index, q_start) pairs, host-packed.
@@ -45,7 +48,13 @@ constexpr int PM = 128;          // query rows per tile (MMA M = TMEM lanes)
 constexpr int PTILES = 2;        // query tiles per CTA, ping-ponged on the tensor core
 constexpr int PBK = 128;         // keys per block (MMA N of S, MMA K of P.V)
 constexpr int PRING = 5;         // K/V block ring (K_j, V_j, K_j+1, ...): 2.5 blocks of prefetch
-constexpr int PF_THREADS = 320;  // warps 0-7 softmax (tile = warp / 4), warp 8 TMA, warp 9 MMA
+// warps 0-7 softmax (tile = warp / 4), warp 8 TMA, warp 9 MMA, warps 10-11 idle: a whole third
+// warpgroup so it can hand registers to the softmax warpgroups (setmaxnreg: 3 warps per SM
+// sub-partition share its 512 registers per lane, 224 + 224 + 56)
+constexpr int PF_THREADS = 384;
+constexpr int PF_REG_SOFTMAX = 200, PF_REG_PRODUCER = 96;
+// the softmax warpgroups' increase must fit in what the producer warpgroup releases (launch: 168 each)
+static_assert(2 * (PF_REG_SOFTMAX - 168) <= 168 - PF_REG_PRODUCER, "setmaxnreg.inc would wait forever");
 constexpr int PF_TMEM_COLS = 512;
 constexpr float RESCALE_TH = 8.f;
 constexpr uint32_t PF_BLK_BYTES = PBK * HD * 2;  // one K or V block: two 64-dim SW128 halves
@@ -57,6 +66,33 @@ struct PrefillSmem {
   uint64_t s_full[PTILES], p_full[PTILES], o_full[PTILES];
   uint32_t tmem_base;
 };
+
+// Timing experiments only (wrong results): MMA K-steps issued per S block / per P.V block.
+#ifndef GLLM_PF_S_STEPS
+#define GLLM_PF_S_STEPS 8
+#endif
+#ifndef GLLM_PF_PV_STEPS
+#define GLLM_PF_PV_STEPS 8
+#endif
+#ifndef GLLM_PF_LOAD_PAGES
+#define GLLM_PF_LOAD_PAGES 64
+#endif
+constexpr int PF_S_STEPS = GLLM_PF_S_STEPS, PF_PV_STEPS = GLLM_PF_PV_STEPS, PF_LOAD_PAGES = GLLM_PF_LOAD_PAGES;
+
+// Debug builds (-DGLLM_TRACE, tools/attn_trace.py): clock64 stamps (relative to the CTA's start)
+// of the prefill pipeline's phases for the first PF_TRACE_CTAS CTAs and PF_TRACE_BLK key blocks.
+#ifdef GLLM_TRACE
+constexpr int PF_TRACE_CTAS = 148, PF_TRACE_BLK = 64, PF_TRACE_EV = 12;
+__device__ unsigned int g_pf_trace[PF_TRACE_CTAS][PF_TRACE_BLK][PF_TRACE_EV];
+#define PF_TRACE(l, ev)                                                                                   \
+  do {                                                                                                    \
+    const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x;                                             \
+    if (lin < PF_TRACE_CTAS && (l) < PF_TRACE_BLK)                                                        \
+      g_pf_trace[lin][(l)][(ev)] = (unsigned)(clock64() - t_cta0);                                        \
+  } while (0)
+#else
+#define PF_TRACE(l, ev) ((void)0)
+#endif
 
 // ---------------------------------------------------------------- decode role
 constexpr int DEC_STAGES = 3;
@@ -368,22 +404,30 @@ GLLM_DEVICE float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
-// P for keys [64h, 64h + 64) of this thread's row: exp2(s * scale - m) packed to bf16 pairs into
-// TMEM columns [32h, 32h + 32) (the S columns of those keys are read before any is overwritten).
-// DIAG: keys c > kmax (after this row's token) are zeroed by position.
+template <int N>
+GLLM_DEVICE void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+GLLM_DEVICE void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
+GLLM_DEVICE float fmax3(float a, float b, float c) {  // FMNMX3 on sm_100
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// P for keys [64h, 64h + 64) of this thread's row from the S values in registers: exp2(s * scale - m)
+// packed to bf16 pairs into TMEM columns [32h, 32h + 32) (every S column was loaded before any P
+// store). DIAG: keys c > kmax (after this row's token) are zeroed by position.
 template <bool DIAG>
-GLLM_DEVICE void softmax_p_half(uint32_t t_s, int h, float2 sc2, float2 ng2, int kmax, float2 (&acc)[2]) {
-  uint32_t s0[32], s1[32], pk[32];
-  tmem_ld_32x32b_x32(t_s + h * 64, s0);
-  tmem_ld_32x32b_x32(t_s + h * 64 + 32, s1);
-  tmem_ld_wait();
+GLLM_DEVICE void softmax_p_half(uint32_t t_s, int h, const uint32_t (&s)[PBK], float2 sc2, float2 ng2, int kmax,
+                                float2 (&acc)[2]) {
+  uint32_t pk[32];
 #pragma unroll
   for (int e = 0; e < 32; ++e) {
-    const uint32_t* sv = e < 16 ? s0 : s1;
-    const float2 x = ffma2(make_float2(__uint_as_float(sv[(2 * e) & 31]), __uint_as_float(sv[(2 * e + 1) & 31])), sc2, ng2);
+    const int c = h * 64 + 2 * e;
+    const float2 x = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, ng2);
     float a = ex2_approx(x.x), b = ex2_approx(x.y);
     if constexpr (DIAG) {
-      const int c = h * 64 + 2 * e;
       a = c <= kmax ? a : 0.f;
       b = c + 1 <= kmax ? b : 0.f;
     }
@@ -416,6 +460,9 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
   PrefillSmem& sm =
       *reinterpret_cast<PrefillSmem*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   constexpr int QT = PM / G;  // query tokens per tile
+#ifdef GLLM_TRACE
+  const long long t_cta0 = clock64();
+#endif
   pdl_trigger();
   pdl_wait();
   const int kvh = blockIdx.x;
@@ -452,7 +499,7 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
     }
     for (int t = 0; t < PTILES; ++t) {
       mbar_init(&sm.s_full[t], 1);
-      mbar_init(&sm.p_full[t], 128);
+      mbar_init(&sm.p_full[t], 4);  // one arrival per softmax warp of the tile
       mbar_init(&sm.o_full[t], 1);
     }
     fence_barrier_init();
@@ -478,27 +525,37 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-
+  if (warp >= 8) {
+  setmaxnreg_dec<PF_REG_PRODUCER>();
   if (warp == 8) {
-    // ---- TMA producer: fill f = 2j loads K_j, f = 2j+1 loads V_j
-    if (lane == 0) {
-      const int n_pages = (kv_len + page_size - 1) / page_size;
-      const int ppb = PBK / page_size;
-      const uint32_t box_bytes = (uint32_t)page_size * 128;
-      const uint64_t pol = policy_evict_last();  // every query tile of the sequence re-reads these pages
-      for (int f = 0; f < 2 * nbl; ++f) {
-        const int s = f % PRING;
-        if (f >= PRING) mbar_wait(&sm.kv_empty[s], ((f / PRING) + 1) & 1);
-        mbar_arrive_expect_tx(&sm.kv_full[s], PF_BLK_BYTES);
-        const CUtensorMap* m = (f & 1) ? &v_map : &k_map;
+    // ---- TMA producer: fill f = 2j loads K_j, f = 2j+1 loads V_j. Lane pl < ppb owns page pl of
+    // every block and issues its two 64-dim boxes; its page id is read from the block table one
+    // block ahead, so no table load sits between a slot's release and its refill.
+    const int n_pages = (kv_len + page_size - 1) / page_size;
+    const int ppb = PBK / page_size;
+    const int ppl = min(ppb, PF_LOAD_PAGES);
+    const uint32_t box_bytes = (uint32_t)page_size * 128;
+    const uint64_t pol = policy_evict_last();  // every query tile of the sequence re-reads these pages
+    // pages past the item's last key repeat its last page (never an unmapped table entry)
+    auto page_row = [&](int j) {
+      return lane < ppl ? (table[min(j * ppb + lane, n_pages - 1)] * n_kv + kvh) * page_size : 0;
+    };
+    int row_cur = nbl > 0 ? page_row(jb) : 0;
+    int row_next = nbl > 1 ? page_row(jb + 1) : 0;
+    for (int f = 0; f < 2 * nbl; ++f) {
+      const int s = f % PRING;
+      if (f >= PRING) mbar_wait(&sm.kv_empty[s], ((f / PRING) + 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&sm.kv_full[s], PF_BLK_BYTES / (ppb / ppl));
+      __syncwarp();
+      const CUtensorMap* m = (f & 1) ? &v_map : &k_map;
+      if (lane < ppl) {
+        tma_load_2d_hint(m, &sm.kv_full[s], sm.kv[s][0] + lane * box_bytes, 0, row_cur, pol);
+        tma_load_2d_hint(m, &sm.kv_full[s], sm.kv[s][1] + lane * box_bytes, 64, row_cur, pol);
+      }
+      if (f & 1) {
         const int j = jb + (f >> 1);
-        for (int pl = 0; pl < ppb; ++pl) {
-          // pages past the item's last key repeat its last page (never an unmapped table entry)
-          const int p = min(j * ppb + pl, n_pages - 1);
-          const int row0 = (table[p] * n_kv + kvh) * page_size;
-          tma_load_2d_hint(m, &sm.kv_full[s], sm.kv[s][0] + pl * box_bytes, 0, row0, pol);
-          tma_load_2d_hint(m, &sm.kv_full[s], sm.kv[s][1] + pl * box_bytes, 64, row0, pol);
-        }
+        row_cur = row_next;
+        row_next = j + 2 < jb + nbl ? page_row(j + 2) : 0;
       }
     }
   } else if (warp == 9) {
@@ -517,7 +574,7 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       const int s = (2 * l) % PRING;
       if (lane == 0) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
+        for (int kk = 0; kk < PF_S_STEPS; ++kk) {
           const uint64_t da = smem_desc_sw128(sm.q[t][kk >> 2]) + 2 * (kk & 3);
           const uint64_t db = smem_desc_sw128(sm.kv[s][kk >> 2]) + 2 * (kk & 3);
           mma_bf16_ss(tmem + t * 256, da, db, idesc_s, kk > 0 ? 1u : 0u);
@@ -526,11 +583,12 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int t, int l) {  // O_t += P_t . V of local block l, P (bf16) in S_t's first 64 columns
+    // O_t += P_t . V of local block l, P (bf16) in S_t's first 64 columns
+    auto issue_pv = [&](int t, int l) {
       const int s = (2 * l + 1) % PRING;
       if (lane == 0) {
 #pragma unroll
-        for (int kk = 0; kk < PBK / 16; ++kk) {
+        for (int kk = 0; kk < PF_PV_STEPS; ++kk) {
           const uint64_t db = smem_desc_sw128_mn(sm.kv[s][0] + kk * 2048, PBK * 128);
           mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, db, idesc_o, (l > 0 || kk > 0) ? 1u : 0u);
         }
@@ -545,7 +603,9 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
     }
     for (int l = 0; l < nbl; ++l) {
       const int j = jb + l;
+      if (lane == 0) PF_TRACE(l, 8);
       wait_full(2 * l + 1);
+      if (lane == 0) PF_TRACE(l, 9);
       if (j == nb - 1 && kv_len < nb * PBK) {
         // keys past the item's last query are never attended, but stale cache slots may hold
         // NaN/Inf bytes and P = 0 times NaN would poison O: zero those V rows
@@ -559,14 +619,20 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
         __syncwarp();
       }
       const bool next = l + 1 < nbl;
-      if (next) wait_full(2 * l + 2);
+      bool k_next = false;  // K_{l+1} is awaited only right before the first S that reads it
       for (int t = 0; t < PTILES; ++t) {
         if (l >= tb[t]) continue;
         mbar_wait(&sm.p_full[t], (uint32_t)(l & 1));
         tc_fence_after();
+        if (lane == 0) PF_TRACE(l, 10 + t);
         issue_pv(t, l);
         if (l + 1 < tb[t]) {
+          if (!k_next) {
+            wait_full(2 * l + 2);
+            k_next = true;
+          }
           issue_s(t, l + 1);
+          if (lane == 0 && t == 0) PF_TRACE(l, 6);
         } else {
           if (lane == 0) mma_commit(&sm.o_full[t]);
           __syncwarp();
@@ -574,8 +640,11 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
       }
       release(2 * l + 1);
       if (next) release(2 * l + 2);
+      if (lane == 0) PF_TRACE(l, 7);
     }
+  }
   } else {
+    setmaxnreg_inc<PF_REG_SOFTMAX>();
     // ---- softmax + epilogue of tile t: this thread owns TMEM lane / query row `row`
     const int t = warp >> 2;
     const int tnq = t ? nq[1] : nq[0], tnb = t ? tb[1] : tb[0];
@@ -591,31 +660,25 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
         const int j = jb + l;
         mbar_wait(&sm.s_full[t], (uint32_t)(l & 1));
         tc_fence_after();
-        // pass 1: row max over the block (diagonal blocks mask keys after this row's token by
-        // position, so stale bytes in unattended slots never reach the max)
+        if (row == 0) PF_TRACE(l, 3 * t);
+        // one pass: the row's 128 S values in registers; diagonal blocks mask keys after this row's
+        // token by position, so stale bytes in unattended slots never reach the max
         const bool diag = (j + 1) * PBK - 1 > qfirst;
         const int kmax = qpos - j * PBK;  // keys c <= kmax are attended
-        // (4 independent max chains: a single fmax chain over 128 keys is latency-bound)
+        uint32_t sv[PBK];
+#pragma unroll
+        for (int c = 0; c < PBK; c += 32) tmem_ld_32x32b_x32(t_s + c, *reinterpret_cast<uint32_t(*)[32]>(&sv[c]));
+        tmem_ld_wait();
+        if (diag) {
+#pragma unroll
+          for (int c = 0; c < PBK; ++c) sv[c] = c <= kmax ? sv[c] : __float_as_uint(-FLT_MAX);
+        }
+        // 4 independent 3-input max chains (one chain over 128 keys is latency-bound)
         float mx[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
-#pragma unroll 1
-        for (int c0 = 0; c0 < PBK; c0 += 64) {
-          uint32_t s0[32], s1[32];
-          tmem_ld_32x32b_x32(t_s + c0, s0);
-          tmem_ld_32x32b_x32(t_s + c0 + 32, s1);
-          tmem_ld_wait();
-          if (diag) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              mx[c & 1] = fmaxf(mx[c & 1], c0 + c <= kmax ? __uint_as_float(s0[c]) : -FLT_MAX);
-              mx[2 + (c & 1)] = fmaxf(mx[2 + (c & 1)], c0 + 32 + c <= kmax ? __uint_as_float(s1[c]) : -FLT_MAX);
-            }
-          } else {
+        for (int c = 0; c < PBK; c += 8) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              mx[c & 1] = fmaxf(mx[c & 1], __uint_as_float(s0[c]));
-              mx[2 + (c & 1)] = fmaxf(mx[2 + (c & 1)], __uint_as_float(s1[c]));
-            }
-          }
+          for (int k = 0; k < 4; ++k) mx[k] = fmax3(mx[k], __uint_as_float(sv[c + 2 * k]), __uint_as_float(sv[c + 2 * k + 1]));
         }
         float mb = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
         mb *= scale_log2;
@@ -639,20 +702,24 @@ attn_prefill_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_cons
             tmem_st_32x32b_x32(t_o + c, o);
           }
         }
-        // pass 2: P = exp2(s * scale - m) as packed bf16 over S's first 64 columns
+        if (row == 0) PF_TRACE(l, 3 * t + 1);
+        // P = exp2(s * scale - m) as packed bf16 over S's first 64 columns, published per half
         float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         const float2 sc2 = make_float2(scale_log2, scale_log2), ng2 = make_float2(-m_ref, -m_ref);
         if (diag) {
-          softmax_p_half<true>(t_s, 0, sc2, ng2, kmax, acc);
-          softmax_p_half<true>(t_s, 1, sc2, ng2, kmax, acc);
+          softmax_p_half<true>(t_s, 0, sv, sc2, ng2, kmax, acc);
+          softmax_p_half<true>(t_s, 1, sv, sc2, ng2, kmax, acc);
         } else {
-          softmax_p_half<false>(t_s, 0, sc2, ng2, kmax, acc);
-          softmax_p_half<false>(t_s, 1, sc2, ng2, kmax, acc);
+          softmax_p_half<false>(t_s, 0, sv, sc2, ng2, kmax, acc);
+          softmax_p_half<false>(t_s, 1, sv, sc2, ng2, kmax, acc);
         }
         l_sum += (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
+        // one arrival per warp once its lanes' P stores completed (4 arrivals, not 128)
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&sm.p_full[t]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.p_full[t]);
+        if (row == 0) PF_TRACE(l, 3 * t + 2);
       }
       if (n_split > 1) {
         // unnormalised partial: O (fp32), running max m (log2 units) and row sum of this split
@@ -1005,3 +1072,12 @@ int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n
 }
 
 }  // namespace gllm
+
+#ifdef GLLM_TRACE
+// debug builds only (not in include/gllm.h): copy the prefill trace [148][64][12] u32 to host
+extern "C" __attribute__((visibility("default"))) int gllm_debug_attn_trace_read(void* host, size_t bytes) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, gllm::g_pf_trace,
+                              bytes < sizeof(gllm::g_pf_trace) ? bytes : sizeof(gllm::g_pf_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -1,0 +1,117 @@
+// Cycles of the prefill softmax's exp phase for one 128-key row block (one thread per row, the
+// row's 128 scores in registers), as the attention kernel runs it: x = s * scale - m (FFMA2),
+// 2^x (MUFU.EX2, or the FMA-pipe polynomial for EMU of every 32 pairs), row sum (FADD2), bf16x2
+// pack (F2FP). W warps per SM; prints cycles per row block per warp.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/softmax_probe tools/softmax_probe.cu
+#include <cstdio>
+#include <cuda_bf16.h>
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  constexpr float MAGIC = 12582912.f;
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 r = fadd2(x, make_float2(MAGIC, MAGIC));
+  const float2 j = fadd2(r, make_float2(-MAGIC, -MAGIC));
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 p = ffma2(f, make_float2(5.500893e-2f, 5.500893e-2f), make_float2(2.4221096e-1f, 2.4221096e-1f));
+  p = ffma2(p, f, make_float2(6.9328293e-1f, 6.9328293e-1f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
+}
+__device__ __forceinline__ unsigned pack(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<unsigned*>(&h);
+}
+
+template <int EMU>
+__global__ void __launch_bounds__(256, 1) probe(const float* in, unsigned* out, long long* cyc, int reps) {
+  float s[128];
+  for (int i = 0; i < 128; ++i) s[i] = in[(threadIdx.x * 7 + i) & 4095];
+  const float2 sc2 = make_float2(0.127f, 0.127f);
+  unsigned pk[64];
+  float lsum = 0.f;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    const float2 ng2 = make_float2(-1.f - lsum * 1e-30f, -1.f - lsum * 1e-30f);  // the row max: per block
+    float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+    for (int e = 0; e < 64; ++e) {
+      const float2 x = ffma2(make_float2(s[2 * e], s[2 * e + 1]), sc2, ng2);
+      float a, b;
+      if (EMU > 0 && (e & 31) % (32 / (EMU > 0 ? EMU : 1)) == 0 && (e & 31) / (32 / (EMU > 0 ? EMU : 1)) < EMU) {
+        const float2 y = ex2_poly2(x);
+        a = y.x;
+        b = y.y;
+      } else {
+        a = ex2(x.x);
+        b = ex2(x.y);
+      }
+      acc[e & 1] = fadd2(acc[e & 1], make_float2(a, b));
+      pk[e] = pack(a, b);
+    }
+    lsum += acc[0].x + acc[0].y + acc[1].x + acc[1].y;
+    // keep the packed P live (the kernel stores it to TMEM) and perturb s so the loop is not hoisted
+    unsigned x = 0;
+#pragma unroll
+    for (int e = 0; e < 64; ++e) x ^= pk[e];
+    s[0] += __uint_as_float(x & 0x3f800000u) * 1e-30f;
+  }
+  const long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(lsum) ^ pk[threadIdx.x & 63];
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int EMU>
+void run(int warps) {
+  float* in;
+  unsigned* out;
+  long long* cyc;
+  cudaMalloc(&in, 4096 * 4);
+  cudaMemset(in, 0, 4096 * 4);
+  cudaMalloc(&out, 148 * 512 * 4);
+  cudaMalloc(&cyc, 148 * 8);
+  const int reps = 256;
+  probe<EMU><<<148, warps * 32>>>(in, out, cyc, reps);
+  probe<EMU><<<148, warps * 32>>>(in, out, cyc, reps);
+  cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+  printf("EMU %2d/32 pairs, warps/SM %2d: %6.0f cycles per 128-key row block per warp (%5.2f P/clk/SM)\n", EMU, warps,
+         (double)mx / reps, (double)warps * 32 * 128 * reps / mx);
+  cudaFree(in);
+  cudaFree(out);
+  cudaFree(cyc);
+}
+
+int main() {
+  for (int w : {4, 8}) {
+    run<0>(w);
+    run<2>(w);
+    run<4>(w);
+    run<8>(w);
+  }
+  return 0;
+}
