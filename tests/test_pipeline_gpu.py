@@ -108,7 +108,10 @@ PP_CONFIGS = {
     "c3_pp4": ["--model", "qwen2.5-14b", "--gpus", "4", "--layers", "8"],
     "c4_pp4_throttle": ["--model", "qwen2.5-32b", "--gpus", "4", "--layers", "8", "--scheduler", "throttle"],
     "c4_pp4_sarathi": ["--model", "qwen2.5-32b", "--gpus", "4", "--layers", "8", "--scheduler", "sarathi"],
-    "c5_pp8": ["--model", "llama3.1-70b", "--gpus", "8", "--layers", "8", "--trace", "c5", "--rate", "4"],
+    # 4-8k prompts: warm in until the first prompts finished and decodes run (the timed window must
+    # hold output tokens)
+    "c5_pp8": ["--model", "llama3.1-70b", "--gpus", "8", "--layers", "8", "--trace", "c5", "--rate", "4",
+               "--warm-max-iters", "60", "--warm-decodes", "8"],
 }
 
 
@@ -126,9 +129,9 @@ def test_bench_pipeline_configs_one_gpu(cuda_ok, name):
     port = s.getsockname()[1]
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", f"--master-port={port}", "bench.py", *args,
+           "--master-addr", "127.0.0.1", f"--master-port={port}", "bench.py",
            "--n-requests", "48", "--steps", "4", "--warmup", "3", "--warm-max-iters", "6", "--profile-steps", "3",
-           "--no-cpu-baseline"]
+           "--no-cpu-baseline", *args]   # the config's own flags last: they override the defaults
     env = dict(os.environ, GLLM_PP_TRANSPORT="host")
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
     rank0 = "\n".join(ln for ln in r.stderr.splitlines() if "[rank0]" in ln or "Error" in ln)

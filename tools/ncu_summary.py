@@ -10,9 +10,11 @@ KEYS = [
     ("dram__bytes_write.sum", "dram write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput % of peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
-    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
-    ("sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed", "bf16 tensor ops % of peak"),
-    ("sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "tc pipe inst %"),
+    # tcgen05 (UMMA) utilisation on sm_100: the hmma sub-pipe's active cycles (the "bf16 tensor ops"
+    # and instruction-count counters read ~0 for tcgen05.mma issued by one thread)
+    ("sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active", "UMMA (tcgen05) pipe active % (active cycles)"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe active % (elapsed)"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem read by tensor pipe % of peak"),
     ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tc pipe cycles %"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("sm__warps_active.avg.per_cycle_active", "warps active / SM"),
