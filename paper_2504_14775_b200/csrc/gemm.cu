@@ -143,8 +143,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tmem_lane_base, int row, 
         for (int j = 0; j < 16; ++j) {
           float a0 = bf2f(f2bf(__uint_as_float(g[2 * j]) * rs)), a1 = bf2f(f2bf(__uint_as_float(g[2 * j + 1]) * rs));
           const float b0 = bf2f(f2bf(__uint_as_float(u[2 * j]) * rs)), b1 = bf2f(f2bf(__uint_as_float(u[2 * j + 1]) * rs));
-          a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
-          a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
+          a0 = bf2f(f2bf(silu_f(a0)));
+          a1 = bf2f(f2bf(silu_f(a1)));
           packed[j] = pack_bf16x2(a0 * b0, a1 * b1);
         }
         uint4* dst = reinterpret_cast<uint4*>(C + (size_t)row * ldc + ocol);
@@ -486,8 +486,8 @@ __global__ void splitk_reduce_swiglu(const float* __restrict__ partial, int spli
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float a0 = bf2f(f2bf(g[2 * j] * rs)), a1 = bf2f(f2bf(g[2 * j + 1] * rs));
-    a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
-    a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
+    a0 = bf2f(f2bf(silu_f(a0)));
+    a1 = bf2f(f2bf(silu_f(a1)));
     pk[j] = pack_bf16x2(a0 * bf2f(f2bf(u[2 * j] * rs)), a1 * bf2f(f2bf(u[2 * j + 1] * rs)));
   }
   *reinterpret_cast<uint4*>(C + (size_t)row * ldc + o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);

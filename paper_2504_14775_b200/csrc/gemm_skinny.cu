@@ -135,8 +135,8 @@ __device__ __forceinline__ void skinny_epilogue(const float* st, int et, int t, 
         float a0 = bf2f(f2bf(st[m * LD + c + 2 * j] * rs)), a1 = bf2f(f2bf(st[m * LD + c + 2 * j + 1] * rs));
         const float b0 = bf2f(f2bf(st[m * LD + 64 + c + 2 * j] * rs)),
                     b1 = bf2f(f2bf(st[m * LD + 64 + c + 2 * j + 1] * rs));
-        a0 = bf2f(f2bf(a0 / (1.f + __expf(-a0))));
-        a1 = bf2f(f2bf(a1 / (1.f + __expf(-a1))));
+        a0 = bf2f(f2bf(silu_f(a0)));
+        a1 = bf2f(f2bf(silu_f(a1)));
         pk[j] = pack_bf16x2(a0 * b0, a1 * b1);
       }
       *reinterpret_cast<uint4*>(C + (size_t)m * ldc + t * 64 + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);

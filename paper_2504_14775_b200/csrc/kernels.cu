@@ -276,7 +276,7 @@ __global__ void silu_mul_kernel(const bf16* __restrict__ gu, int d_ff, bf16* __r
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float2 a = unpack_bf16x2(ga[j]), b = unpack_bf16x2(ua[j]);
-    float s0 = bf2f(f2bf(a.x / (1.f + __expf(-a.x)))), s1 = bf2f(f2bf(a.y / (1.f + __expf(-a.y))));
+    float s0 = bf2f(f2bf(silu_f(a.x))), s1 = bf2f(f2bf(silu_f(a.y)));
     o[j] = pack_bf16x2(s0 * b.x, s1 * b.y);
   }
   *reinterpret_cast<uint4*>(out + r * d_ff + c) = make_uint4(o[0], o[1], o[2], o[3]);

@@ -24,6 +24,7 @@ def _rel(a, b):
 GEMM_SHAPES = [
     (1, 512, 256), (7, 256, 256), (64, 1536, 256), (128, 512, 4096), (130, 4096, 4096),
     (300, 6144, 4096), (1000, 4096, 14336), (33, 28672, 4096), (2048, 4096, 4096),
+    (2009, 6144, 4096),   # 192 2-CTA tiles over 74 clusters: 44-tile stream-K tail
 ]
 
 
@@ -82,7 +83,8 @@ def test_gemm_skinny_stream_k(lib, M, N, K):
     assert torch.equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096)])
+@pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096),
+                                   (2009, 6144, 4096), (1500, 8192, 8192)])
 def test_gemm_deterministic(lib, M, N, K):
     """Auto tiling (incl. split-K partial sums) is bit-stable across runs and agrees with whole-tile
     (force_splits=1) tiling to fp32 rounding."""

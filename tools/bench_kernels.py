@@ -85,9 +85,9 @@ def attn_case(name, seqs, n_heads=32, n_kv=8, ps=16, force_mixed=False, split=1,
                       "hbm_frac": round(kv_bytes / ms / 1e6 / PEAK["hbm_gbs"], 3), "TFLOP/s": round(flops / ms / 1e9, 1)}))
 
 
-def gemm_case(M, N, K, bn=0, splits=0, swiglu=False):
+def gemm_case(M, N, K, bn=0, splits=0, swiglu=False, wscale=1.0):
     A = torch.randn(M, K, device="cuda").bfloat16()
-    B = torch.randn(N, K, device="cuda").bfloat16()
+    B = (torch.randn(N, K, device="cuda") * wscale).bfloat16()
     C = torch.empty(M, N, device="cuda").bfloat16()
     ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
     st = native.stream_handle()
@@ -110,12 +110,13 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--case", default="")
+    ap.add_argument("--wscale", type=float, default=1.0, help="weight std (0.02 = the stages' init)")
     ap.add_argument("--gemm", default="", help="M,N,K[,bn,splits] single GEMM case (bn/splits 0 = auto)")
     ap.add_argument("--swiglu", action="store_true")
     a = ap.parse_args()
     if a.gemm:
         v = [int(x) for x in a.gemm.split(",")] + [0, 0]
-        gemm_case(v[0], v[1], v[2], bn=v[3], splits=v[4], swiglu=a.swiglu)
+        gemm_case(v[0], v[1], v[2], bn=v[3], splits=v[4], swiglu=a.swiglu, wscale=a.wscale)
         raise SystemExit(0)
     if a.case:
         _orig = attn_case

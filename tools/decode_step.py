@@ -39,9 +39,10 @@ def main():
 
     spec = MODELS[a.model]
     warm = 40
-    # the first prompts finish prefill ~batch*ctx/2048 iterations before the last: their outputs
-    # must outlast that, or the batch never runs full decode-only steps
-    pf_iters = -(-a.batch * a.ctx // 2048) + 8
+    # the first prompts finish prefill up to ~batch*ctx/2048 iterations before the last, plus the
+    # throttled tail (#P = #WP/T once #WP < T*MaxP: ~T*ln(T*MaxP/MinP) more iterations): their
+    # outputs must outlast that, or the batch never runs full decode-only steps
+    pf_iters = -(-a.batch * a.ctx // 2048) + 96
     reqs = [RequestSpec(i, 0.0, a.ctx, warm + a.steps + 8 + pf_iters) for i in range(a.batch)]
     pages = a.batch * (-(-(a.ctx + warm + a.steps + 16 + pf_iters) // 16)) + 64
     ex = LocalExecutor(spec, reqs, num_pages=pages, page_size=16, max_tokens=2048, max_emit=max(a.batch, 32), seed=0,

@@ -4,7 +4,8 @@ the serving M range: decode batches, medium mixed batches and full 2k-token micr
     python tools/gemm_sweep.py [--m 4,16,64,128,256,512,1024,2009] [--out gpurun_out/gemm_sweep.csv]
 
 Gate-up runs through the fused SwiGLU entry point (its output is N/2 wide); cuBLAS does the plain
-[M, K] x [K, N] product. L2 is flushed between reps (tools/bench_kernels.timeit).
+[M, K] x [K, N] product. Weights are N(0, 0.02^2) like the stages' init, activations N(0, 1). L2 is
+flushed between reps (tools/bench_kernels.timeit).
 """
 import argparse
 import csv
@@ -43,7 +44,7 @@ def main():
     for cfg, model in CONFIGS:
         spec = MODELS[model]
         for name, N, K, swiglu in shapes(spec):
-            B = torch.randn(N, K, device="cuda").bfloat16()
+            B = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
             for M in ms_list:
                 if name == "lm_head" and M > 1024:
                     continue
