@@ -29,11 +29,14 @@ def main():
     ap.add_argument("--ctx", type=int, default=512)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--cuda-graphs", action="store_true", help="decode-only batches as captured CUDA graphs")
+    ap.add_argument("--profile", action="store_true",
+                    help="per-kernel-class device time of the timed steps (native CUDA-event profiler; "
+                         "its events serialise the launches, so ms_per_step is then not the clean figure)")
     a = ap.parse_args()
 
     import torch
 
-    from paper_2504_14775_b200 import Engine, KvConfig, PipelineConfig, RequestSpec, ThrottleConfig
+    from paper_2504_14775_b200 import Engine, KvConfig, PipelineConfig, RequestSpec, ThrottleConfig, native
     from paper_2504_14775_b200.executor import LocalExecutor
     from paper_2504_14775_b200.modelspec import MODELS
 
@@ -58,10 +61,13 @@ def main():
             if len(decode_only) == warm // 2 and not ranged:
                 torch.cuda.synchronize()
                 torch.cuda.nvtx.range_push("decode_timed")
+                if a.profile:
+                    native.profile_begin()
                 ranged = True
             if len(decode_only) >= warm // 2 + a.steps:
                 break
     torch.cuda.synchronize()
+    prof = native.profile_end() if (ranged and a.profile) else None
     if ranged:
         torch.cuda.nvtx.range_pop()
     for _ in range(8):  # retire the last timed batches (their device times are read at retirement)
@@ -84,6 +90,13 @@ def main():
                       "graph_replays": ex.graph_replays, "steps": len(ms), "ms_per_step": round(med, 3),
                       "wall_ms_per_step": round(wall_ms, 3) if wall_ms else None,
                       "weight_floor_ms": round(floor_ms, 3), "frac_of_floor": round(floor_ms / med, 3)}))
+    if prof:
+        n = max(1, len(decode_only) - warm // 2)
+        for name, e in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"]):
+            us = e["total_ms"] * 1e3 / max(1, e["launches"])
+            gbs = e["bytes"] / (e["total_ms"] * 1e6) if e["total_ms"] else 0.0
+            print(f"  {name:14s} {e['total_ms'] / n:7.3f} ms/step  {e['launches'] // n:4d} launches/step  "
+                  f"{us:8.1f} us/launch  {gbs:7.0f} GB/s algorithmic")
 
 
 if __name__ == "__main__":
