@@ -545,7 +545,7 @@ def emit_ours(args, dd: _Dist, res: dict) -> dict:
         "metric": "output_tokens_per_s", "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
         "steps": K, "warmup": 0 if args.whole_trace else args.warmup,
         "ms_per_step": round(res["wall_s"] * 1000 / K, 3),
-        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, seeded trace, PCG64 prompt tokens)",
         "config": config_dict(args, world),
@@ -592,7 +592,7 @@ def run_reference(args, world: int) -> dict:
                      time_budget_s=240.0, warm_decodes=args.warm_decodes, warm_max_iters=args.warm_max_iters)
     return {"metric": "output_tokens_per_s", "value": r["value"], "unit": "tokens/s", "n_gpus": 0,
             "steps": r["steps"], "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
-            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (random-init weights, seeded trace, PCG64 prompt tokens)",
             "config": config_dict(args, world),
             "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
