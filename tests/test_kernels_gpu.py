@@ -83,6 +83,31 @@ def test_gemm_skinny_stream_k(lib, M, N, K):
     assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("M,N,K", [(64, 5120, 5120), (33, 4096, 4096), (100, 4096, 14336), (128, 5120, 13824),
+                                   (64, 8192, 8192), (48, 6144, 4096)])
+def test_gemm_one_row_tile(lib, M, N, K):
+    """One row tile (33-128 tokens, the medium decode batches): the auto plan (whole-K narrow tiles or
+    split-K + reduce) with bias + residual against fp32, bit-stable across runs, and the forced
+    whole-K plan."""
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, K, device="cuda", generator=g) * 0.02).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g).bfloat16()
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    ws = torch.empty(160 << 20, dtype=torch.uint8, device="cuda")
+    outs = []
+    for splits in (0, 0, 1):
+        C_ = torch.full((M, N), float("nan"), device="cuda").bfloat16()
+        lib.call("gllm_gemm_bf16", A.data_ptr(), K, B.data_ptr(), K, C_.data_ptr(), N, M, N, K, bias.data_ptr(),
+                 res.data_ptr(), N, 0, splits, ws.data_ptr(), ws.numel(), lib.stream_handle())
+        outs.append(C_)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T + bias.float() + res.float()
+    assert torch.isfinite(outs[0].float()).all()
+    assert _rel(outs[0], ref) < 8e-3 and _rel(outs[2], ref) < 8e-3
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096),
                                    (2009, 6144, 4096), (1500, 8192, 8192)])
 def test_gemm_deterministic(lib, M, N, K):
