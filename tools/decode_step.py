@@ -5,8 +5,8 @@
 N requests (prompt --ctx tokens, long outputs) all arrive at t=0; the virtual-clock engine
 (reference scheduling) drives LocalExecutor until every request decodes, then the device time
 of each decode-only micro-batch (N tokens, no prefill) is read from CUDA events. Prints the
-median ms per step and its ratio to the weight-streaming floor (stage weights / measured HBM
-bandwidth). Run under `ncu --nvtx --nvtx-include decode_timed/` for a per-kernel split.
+median ms per step and its ratio to the HBM floor (stage weights + the batch's KV-cache reads at
+the mid-window context, over the measured HBM bandwidth). Run under `ncu --nvtx --nvtx-include decode_timed/` for a per-kernel split.
 """
 
 from __future__ import annotations
@@ -81,7 +81,10 @@ def main():
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except (OSError, KeyError, ValueError):
         hbm = 6650.0
-    floor_ms = w_bytes / (hbm * 1e9) * 1e3
+    # every decode also reads its KV cache: batch x context (mid-window) x layers x KV bytes
+    ctx_mid = a.ctx + pf_iters // 2 + warm // 2 + a.steps // 2
+    kv_bytes = a.batch * ctx_mid * spec.n_layers * spec.kv_bytes_per_token_layer
+    floor_ms = (w_bytes + kv_bytes) / (hbm * 1e9) * 1e3
     med = statistics.median(ms)
     # host wall time per decode step through the engine (planning, packing, launches, token read-back)
     gaps = [b - a_ for a_, b in zip(wall[warm // 2:], wall[warm // 2 + 1:])]
@@ -89,7 +92,8 @@ def main():
     print(json.dumps({"model": a.model, "batch": a.batch, "ctx": a.ctx, "cuda_graphs": a.cuda_graphs,
                       "graph_replays": ex.graph_replays, "steps": len(ms), "ms_per_step": round(med, 3),
                       "wall_ms_per_step": round(wall_ms, 3) if wall_ms else None,
-                      "weight_floor_ms": round(floor_ms, 3), "frac_of_floor": round(floor_ms / med, 3)}))
+                      "floor_ms": round(floor_ms, 3), "kv_gb": round(kv_bytes / 1e9, 2),
+                      "frac_of_floor": round(floor_ms / med, 3)}))
     if prof:
         n = max(1, len(decode_only) - warm // 2)
         for name, e in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"]):
