@@ -56,6 +56,8 @@ def main() -> int:
     ap.add_argument("--layers", type=int, default=0, help="test only: truncate the model")
     ap.add_argument("--max-pages", type=int, default=0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--max-wall-s", type=float, default=0.0,
+                    help="stop a run cleanly after this much host time (the row is marked truncated)")
     a = ap.parse_args()
 
     import torch
@@ -111,7 +113,16 @@ def main() -> int:
                          kv_config=KvConfig(num_pages, page), throttle=ThrottleConfig(), executor=ex,
                          measured_stage_times=True)
             t0 = time.perf_counter()
-            raw = eng.run()
+            truncated = False
+            if a.max_wall_s:
+                while eng.step():
+                    if time.perf_counter() - t0 > a.max_wall_s:
+                        truncated = True
+                        break
+                torch.cuda.synchronize()
+                raw = eng.raw_data()
+            else:
+                raw = eng.run()
             wall = time.perf_counter() - t0
             rep = build_report(raw)
             stage_busy = [sum(b - s for s, b in ivs) for ivs in raw.busy_intervals]
@@ -130,7 +141,7 @@ def main() -> int:
                    "hop": f"modelled {a.hop_latency_ms} ms + N_tok*{spec.d_model * 2} B / {a.hop_gbs} GB/s",
                    "method": "measured-time replay on 1 B200: every stage executed and CUDA-event timed; "
                              "pipeline timeline = reference event loop over the measured stage times",
-                   "host_wall_s": round(wall, 1)}
+                   "host_wall_s": round(wall, 1), "truncated": truncated}
             rows.append(row)
             print(json.dumps(row), flush=True)
     if a.out:
