@@ -302,10 +302,32 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
 
   if (warp == 0) {
     if (elect_one()) {
-      pdl_wait();  // A is the predecessor's output
       const uint64_t pol_w = policy_evict_first();  // weights stream through once per step
       // both CTAs' loads complete on the leader's `full` barrier (CG = 2)
       const uint32_t full_leader = CG == 2 ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+      auto expect = [&](int s) {
+        if constexpr (CG == 1) mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES - (BM - a_box) * BK * 2);
+        else if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+      };
+      auto load_b = [&](int s, int kc, int bn) {
+        uint8_t* sb = smem + s * L::STAGE_BYTES + L::A_BYTES;
+        if constexpr (CG == 1) tma_load_2d_hint(&map_b, &full[s], sb, kc, bn, pol_w);
+        else tma_load_2d_cg2(&map_b, full_leader + (uint32_t)(s * 8), sb, kc, bn, pol_w);
+      };
+      // The weights (B) do not depend on the predecessor kernel: the first ring's worth of this
+      // CTA's first unit is fetched before griddepcontrol.wait, so the weight stream overlaps the
+      // predecessor's tail; only the activations (A) wait for it.
+      int pre = 0;
+      if (unit0 < units) {
+        int m0, n0, split, kb0, nkb;
+        unit_coords(unit0, m0, n0, split, kb0, nkb);
+        pre = min(nkb, STAGES);
+        for (int i = 0; i < pre; ++i) {
+          expect(i);
+          load_b(i, (kb0 + i) * BK, n0 + (int)rank * (BN / CG));
+        }
+      }
+      pdl_wait();  // A is the predecessor's output
       int it = 0;
       for (int u = unit0; u < units; u += ustride) {
         int m0, n0, split, kb0, nkb;
@@ -314,20 +336,15 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a, const __grid_consta
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
-          uint8_t* sb = sa + L::A_BYTES;
           const int kc = (kb0 + i) * BK;
-          if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES - (BM - a_box) * BK * 2);
-            tma_load_2d(&map_a, &full[s], sa, kc, am);
-            tma_load_2d_hint(&map_b, &full[s], sb, kc, bn, pol_w);
-          } else {
-            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * L::STAGE_BYTES);
-            const uint32_t bar = full_leader + (uint32_t)(s * 8);
-            tma_load_2d_cg2(&map_a, bar, sa, kc, am, policy_evict_last());
-            tma_load_2d_cg2(&map_b, bar, sb, kc, bn, pol_w);
+          if (it >= pre) {
+            mbar_wait(&empty[s], ph ^ 1);
+            expect(s);
+            load_b(s, kc, bn);
           }
+          if constexpr (CG == 1) tma_load_2d(&map_a, &full[s], sa, kc, am);
+          else tma_load_2d_cg2(&map_a, full_leader + (uint32_t)(s * 8), sa, kc, am, policy_evict_last());
         }
       }
     }
