@@ -323,3 +323,14 @@ def test_prefix_caching_logits(cuda_ok):
         assert len(ex.outputs[r.id]) == r.output_tokens
     print(f"prefix caching: {eng.kv.hit_tokens} cached prompt tokens reused, worst logits rel err {worst:.3e}")
     assert worst < 2e-2, worst
+
+
+def test_graft_entry_smoke(cuda_ok):
+    """The driver's round-end smoke: one tiny engine run on cuda:0 checked against the fp32 oracle."""
+    import importlib
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if root not in sys.path:
+        sys.path.insert(0, root)
+    importlib.import_module("__graft_entry__").smoke()
