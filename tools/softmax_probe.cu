@@ -5,6 +5,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/softmax_probe tools/softmax_probe.cu
 #include <cstdio>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -38,6 +39,13 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
 }
+// 2^x for a pair with one MUFU op: f16x2 input / output (sm_75+ ex2.approx.f16x2)
+__device__ __forceinline__ float2 ex2_h2(float2 x) {
+  const __half2 h = __floats2half2_rn(x.x, x.y);
+  unsigned u = *reinterpret_cast<const unsigned*>(&h), r;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(u));
+  return __half22float2(*reinterpret_cast<const __half2*>(&r));
+}
 __device__ __forceinline__ unsigned pack(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<unsigned*>(&h);
@@ -59,7 +67,11 @@ __global__ void __launch_bounds__(256, 1) probe(const float* in, unsigned* out, 
     for (int e = 0; e < 64; ++e) {
       const float2 x = ffma2(make_float2(s[2 * e], s[2 * e + 1]), sc2, ng2);
       float a, b;
-      if (EMU > 0 && (e & 31) % (32 / (EMU > 0 ? EMU : 1)) == 0 && (e & 31) / (32 / (EMU > 0 ? EMU : 1)) < EMU) {
+      if (EMU < 0) {
+        const float2 y = ex2_h2(x);
+        a = y.x;
+        b = y.y;
+      } else if (EMU > 0 && (e & 31) % (32 / (EMU > 0 ? EMU : 1)) == 0 && (e & 31) / (32 / (EMU > 0 ? EMU : 1)) < EMU) {
         const float2 y = ex2_poly2(x);
         a = y.x;
         b = y.y;
@@ -99,7 +111,7 @@ void run(int warps) {
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
   long long mx = 0;
   for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-  printf("EMU %2d/32 pairs, warps/SM %2d: %6.0f cycles per 128-key row block per warp (%5.2f P/clk/SM)\n", EMU, warps,
+  printf("EMU %2d/32 pairs (-1 = ex2.f16x2), warps/SM %2d: %6.0f cycles per 128-key row block per warp (%5.2f P/clk/SM)\n", EMU, warps,
          (double)mx / reps, (double)warps * 32 * 128 * reps / mx);
   cudaFree(in);
   cudaFree(out);
@@ -108,6 +120,7 @@ void run(int warps) {
 
 int main() {
   for (int w : {4, 8}) {
+    run<-1>(w);
     run<0>(w);
     run<2>(w);
     run<4>(w);
