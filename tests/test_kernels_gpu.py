@@ -340,6 +340,8 @@ DECODE_SETS = {
     "two_long": (2999, 700),          # few sequences: cluster KV split of up to 4 ranks
     "one_very_long": (8191,),
     "short_and_long": (5, 1500, 40),  # ranks with empty page ranges
+    # 48 decodes x 8 kv heads = 384 items: one wave of three 4-warp CTAs per SM (2-stage page ring)
+    "medium_batch": tuple((37 * i) % 900 for i in range(48)),
 }
 
 
@@ -347,7 +349,8 @@ DECODE_SETS = {
                                                     (40, 8, "mixed_ctx", False), (32, 8, "mixed_ctx", True),
                                                     (64, 8, "two_long", True), (40, 8, "two_long", True),
                                                     (32, 8, "one_very_long", True), (40, 8, "short_and_long", True),
-                                                    (32, 8, "two_long", False)])
+                                                    (32, 8, "two_long", False), (40, 8, "medium_batch", False),
+                                                    (64, 8, "medium_batch", True)])
 def test_attention_decode_only_launch(lib, n_heads, n_kv, ctxs, auto):
     """All-decode micro-batch: the decode-only instantiation (no prefill resources) must agree too;
     `auto` passes the host metadata, so few long sequences take the cluster KV split."""
