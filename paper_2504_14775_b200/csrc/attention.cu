@@ -97,13 +97,13 @@ __device__ unsigned int g_pf_trace[PF_TRACE_CTAS][PF_TRACE_BLK][PF_TRACE_EV];
 // ---------------------------------------------------------------- decode role
 constexpr int DEC_STAGES = 3;
 constexpr int MAX_PAGE_BYTES = 16 * HD * 2;  // page_size <= 16 for the bulk ring
-template <int NW>  // streaming warps per CTA
+template <int NW, int ST = DEC_STAGES>  // streaming warps per CTA, page-ring stages per warp
 struct DecodeSmem {
   union {
-    __align__(128) uint8_t kv[NW][DEC_STAGES][2][MAX_PAGE_BYTES];
+    __align__(128) uint8_t kv[NW][ST][2][MAX_PAGE_BYTES];
     float merge_acc[NW][8][HD];  // reused after every page has been consumed
   };
-  uint64_t full[NW][DEC_STAGES];
+  uint64_t full[NW][ST];
   float merge_m[NW][8];
   float merge_l[NW][8];
 };
@@ -156,7 +156,7 @@ GLLM_DEVICE void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
 // O += P.V (P reused from the S accumulator registers), with the online softmax
 // on quads of lanes (one query head per quad). Warps merge through smem; with a KV split
 // (csize > 1) the ranks of the cluster then merge through rank 0's DecodeRed.
-template <int G, int NW>
+template <int G, int NW, int ST = DEC_STAGES>
 __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok, int kv_len,
                                             const int* __restrict__ table, const CUtensorMap* k_map,
                                             const CUtensorMap* v_map, int n_heads, int n_kv, int kvh,
@@ -164,7 +164,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
                                             int csize = 1, int crank = 0) {
   static_assert(G <= 8, "decode tile holds up to 8 query heads per kv head");
   constexpr int HALF_BYTES = 16 * 128;  // one 64-dim box of a 16-slot page (8-slot pages use half)
-  DecodeSmem<NW>& sm = *reinterpret_cast<DecodeSmem<NW>*>(smem_raw);
+  DecodeSmem<NW, ST>& sm = *reinterpret_cast<DecodeSmem<NW, ST>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qr = lane >> 2;          // fragment row = query head within the group
   const int qc = (lane & 3) * 2;     // fragment column pair
@@ -176,7 +176,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   const int nblk = page_size / 8;    // 8-key MMA n-blocks per page (1 or 2)
 
   if (lane == 0) {
-    for (int s = 0; s < DEC_STAGES; ++s) mbar_init(&sm.full[warp][s], 1);
+    for (int s = 0; s < ST; ++s) mbar_init(&sm.full[warp][s], 1);
     fence_barrier_init();
   }
   __syncwarp();
@@ -198,14 +198,14 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   // by that GEMM's epilogue (and may be newly appended to the table): it waits, as does Q.
   const int p_last = n_pages_all - 1;
   if (lane == 0) {
-    for (int s = 0; s < DEC_STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       const int p = p_begin + warp + s * NW;
       if (p < n_pages && p < p_last) issue(p, s);
     }
   }
   pdl_wait();
   if (lane == 0) {
-    for (int s = 0; s < DEC_STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       const int p = p_begin + warp + s * NW;
       if (p < n_pages && p == p_last) issue(p, s);
     }
@@ -230,8 +230,8 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
 
   int it = 0;
   for (int p = p_begin + warp; p < n_pages; p += NW, ++it) {
-    const int s = it % DEC_STAGES;
-    mbar_wait(&sm.full[warp][s], (uint32_t)((it / DEC_STAGES) & 1));
+    const int s = it % ST;
+    mbar_wait(&sm.full[warp][s], (uint32_t)((it / ST) & 1));
     uint8_t* kp = sm.kv[warp][s][0];
     uint8_t* vp = sm.kv[warp][s][1];
     const int keys_here = min(page_size, kv_len - p * page_size);
@@ -311,7 +311,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
       mma_16816_bf16(o[nb + 1], a_frag, vb[2], vb[3]);
     }
     __syncwarp();
-    const int pn = p + DEC_STAGES * NW;
+    const int pn = p + ST * NW;
     if (lane == 0 && pn < n_pages) {
       fence_proxy_async();
       issue(pn, s);
@@ -332,7 +332,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
     }
   }
   __syncthreads();
-  DecodeRed* red = reinterpret_cast<DecodeRed*>(smem_raw + ((sizeof(DecodeSmem<NW>) + 127) & ~size_t(127)));
+  DecodeRed* red = reinterpret_cast<DecodeRed*>(smem_raw + ((sizeof(DecodeSmem<NW, ST>) + 127) & ~size_t(127)));
   const uint32_t red_leader = csize > 1 ? mapa_shared(smem_u32(red), 0) : 0u;
   for (int i = threadIdx.x; i < G * HD; i += NW * 32) {
     const int h = i / HD, d = i % HD;
@@ -819,8 +819,8 @@ attn_split_combine(const int* __restrict__ seq_info, const int* __restrict__ wor
 // NW = 4 (two CTAs per SM) for large decode populations; NW = 8 (one CTA, twice the pages in
 // flight per sequence) when all (sequence, kv head) items fit in one wave of SMs: small batches
 // are latency-bound on each sequence's page stream.
-template <int G, int NW>
-__global__ void __launch_bounds__(NW * 32, NW == 4 ? 2 : 1)
+template <int G, int NW, int ST = DEC_STAGES>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? (ST == DEC_STAGES ? 2 : 3) : 1)
 attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_constant__ CUtensorMap v_map,
                    const bf16* __restrict__ qkv, const int* __restrict__ seq_info, const int* __restrict__ work,
                    const int* __restrict__ block_table, int mpr, int n_heads, int n_kv, int page_size,
@@ -837,7 +837,7 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap k_map, const __grid_const
   const int* si = seq_info + 5 * sidx;
   const int row_id = si[0], start = si[1], tok_off = si[3];
   const int* table = block_table + (size_t)row_id * mpr;
-  decode_role<G, NW>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh,
+  decode_role<G, NW, ST>(smem_raw, qkv, tok_off + q0, start + q0 + 1, table, &k_map, &v_map, n_heads, n_kv, kvh,
                      page_size, scale_log2, out, csize, crank);
 }
 
@@ -888,13 +888,14 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
                        int dec_pages = 0) {
   constexpr size_t smem_pf = sizeof(PrefillSmem) + 1024;
   constexpr size_t smem4 = sizeof(DecodeSmem<4>) + 1024;
+  constexpr size_t smem4s = sizeof(DecodeSmem<4, 2>) + 1024;   // 3 CTAs per SM
   constexpr size_t smem8 = ((sizeof(DecodeSmem<8>) + 127) & ~size_t(127)) + sizeof(DecodeRed) + 1024;
   static bool attr = false;
   if (!attr) {
-    const void* fns[3] = {(const void*)attn_prefill_kernel<G>, (const void*)attn_decode_kernel<G, 4>,
-                          (const void*)attn_decode_kernel<G, 8>};
-    const size_t sm[3] = {smem_pf, smem4, smem8};
-    for (int i = PREFILL ? 0 : 1; i < (PREFILL ? 1 : 3); ++i) {
+    const void* fns[4] = {(const void*)attn_prefill_kernel<G>, (const void*)attn_decode_kernel<G, 4>,
+                          (const void*)attn_decode_kernel<G, 8>, (const void*)attn_decode_kernel<G, 4, 2>};
+    const size_t sm[4] = {smem_pf, smem4, smem8, smem4s};
+    for (int i = PREFILL ? 0 : 1; i < (PREFILL ? 1 : 4); ++i) {
       cudaError_t e = cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm[i]);
       if (e != cudaSuccess) return set_cuda_error(e, "attention smem attribute");
       // all of the unified L1/smem as shared memory (decode: 8 streaming warps per SM)
@@ -943,9 +944,19 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
         }
     }
     grid.x = n_kv * csize;
+    // Between one and 1.5 waves of two 4-warp CTAs per SM, three CTAs per SM with a 2-stage page
+    // ring (the same pages in flight per SM) keep the items in one wave: e.g. 48-55 decodes with
+    // 8 kv heads (384-440 items) against 296 two-per-SM slots.
+    static const int three = [] {
+      const char* e = getenv("GLLM_DECODE_3CTA");  // A/B switch (default on)
+      return e ? atoi(e) : 1;
+    }();
+    const bool tri = !wide && three && items > 2L * sms && items <= 3L * sms;
     cudaError_t e = wide ? launch_kernel(attn_decode_kernel<G, 8>, grid, dim3(256), smem8, st, csize, km, vm, qkv,
                                          seq_info, work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out,
                                          csize)
+                  : tri  ? launch_kernel(attn_decode_kernel<G, 4, 2>, grid, dim3(128), smem4s, st, 1, km, vm, qkv,
+                                         seq_info, work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out, 1)
                          : launch_kernel(attn_decode_kernel<G, 4>, grid, dim3(128), smem4, st, 1, km, vm, qkv, seq_info,
                                          work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out, 1);
     if (e != cudaSuccess) return set_cuda_error(e, "attention_decode launch");
