@@ -90,8 +90,18 @@ __device__ unsigned int g_pf_trace[PF_TRACE_CTAS][PF_TRACE_BLK][PF_TRACE_EV];
     if (lin < PF_TRACE_CTAS && (l) < PF_TRACE_BLK)                                                        \
       g_pf_trace[lin][(l)][(ev)] = (unsigned)(clock64() - t_cta0);                                        \
   } while (0)
+// decode role: per CTA (first DEC_TRACE_CTAS), warp, page iteration: [wait start, page ready, page done]
+constexpr int DEC_TRACE_CTAS = 296, DEC_TRACE_IT = 32;
+__device__ unsigned int g_dec_trace[DEC_TRACE_CTAS][8][DEC_TRACE_IT][3];
+#define DEC_TRACE(it, ev)                                                                                 \
+  do {                                                                                                    \
+    const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x;                                             \
+    if (lin < DEC_TRACE_CTAS && (it) < DEC_TRACE_IT && lane == 0)                                         \
+      g_dec_trace[lin][warp][(it)][(ev)] = (unsigned)(clock64() - t_cta0);                                \
+  } while (0)
 #else
 #define PF_TRACE(l, ev) ((void)0)
+#define DEC_TRACE(it, ev) ((void)0)
 #endif
 
 // ---------------------------------------------------------------- decode role
@@ -163,6 +173,9 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
                                             int page_size, float scale_log2, bf16* __restrict__ out,
                                             int csize = 1, int crank = 0) {
   static_assert(G <= 8, "decode tile holds up to 8 query heads per kv head");
+#ifdef GLLM_TRACE
+  const long long t_cta0 = clock64();
+#endif
   constexpr int HALF_BYTES = 16 * 128;  // one 64-dim box of a 16-slot page (8-slot pages use half)
   DecodeSmem<NW, ST>& sm = *reinterpret_cast<DecodeSmem<NW, ST>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -231,7 +244,9 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   int it = 0;
   for (int p = p_begin + warp; p < n_pages; p += NW, ++it) {
     const int s = it % ST;
+    DEC_TRACE(it, 0);
     mbar_wait(&sm.full[warp][s], (uint32_t)((it / ST) & 1));
+    DEC_TRACE(it, 1);
     uint8_t* kp = sm.kv[warp][s][0];
     uint8_t* vp = sm.kv[warp][s][1];
     const int keys_here = min(page_size, kv_len - p * page_size);
@@ -316,6 +331,7 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
       fence_proxy_async();
       issue(pn, s);
     }
+    DEC_TRACE(it, 2);
   }
   // ---- merge the 4 warps through smem (rows < G only); the ring is reused, so all
   // warps must be done with their pages first
@@ -1085,6 +1101,12 @@ int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n
 }  // namespace gllm
 
 #ifdef GLLM_TRACE
+// debug builds only (not in include/gllm.h): copy the decode trace [296][8][32][3] u32 to host
+extern "C" __attribute__((visibility("default"))) int gllm_debug_dec_trace_read(void* host, size_t bytes) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(host, gllm::g_dec_trace,
+                              bytes < sizeof(gllm::g_dec_trace) ? bytes : sizeof(gllm::g_dec_trace)) == cudaSuccess ? 0 : -1;
+}
 // debug builds only (not in include/gllm.h): copy the prefill trace [148][64][12] u32 to host
 extern "C" __attribute__((visibility("default"))) int gllm_debug_attn_trace_read(void* host, size_t bytes) {
   cudaDeviceSynchronize();

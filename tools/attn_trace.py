@@ -23,7 +23,34 @@ import bench_kernels as bk  # noqa: E402
 from paper_2504_14775_b200 import native  # noqa: E402
 
 CTAS, BLK, EV = 148, 64, 12
-CASES = {"70b": ([(4096, 2048)], 64), "8b": ([(0, 2048)], 32), "qwen": ([(2000, 512)] * 4, 40)}
+CASES = {"70b": ([(4096, 2048)], 64), "8b": ([(0, 2048)], 32), "qwen": ([(2000, 512)] * 4, 40),
+         # decode role (one query token per sequence)
+         "dec32x512": ([(512, 1)] * 32, 40), "dec48x512": ([(512, 1)] * 48, 40), "dec8x8000": ([(8000, 1)] * 8, 32),
+         "dec800x500": ([(500, 1)] * 800, 32)}
+DEC_CTAS, DEC_W, DEC_IT = 296, 8, 32
+
+
+def decode_report(lib, name):
+    buf = np.zeros((DEC_CTAS, DEC_W, DEC_IT, 3), dtype=np.uint32)
+    fn = lib.gllm_debug_dec_trace_read
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert fn(buf.ctypes.data, buf.nbytes) == 0
+    wait, comp, first, end = [], [], [], []
+    for c in range(DEC_CTAS):
+        for w in range(DEC_W):
+            ev = buf[c, w]
+            n = int(np.count_nonzero(ev[:, 2]))
+            if n == 0:
+                continue
+            first.append(int(ev[0, 1]))
+            end.append(int(ev[n - 1, 2]))
+            for i in range(n):
+                wait.append(int(ev[i, 1]) - int(ev[i, 0]))
+                comp.append(int(ev[i, 2]) - int(ev[i, 1]))
+    print(f"case {name}: warps traced {len(first)}")
+    print(f"  first page ready {med(first):.0f} cyc after CTA start; warp done {med(end):.0f} cyc (max {max(end)})")
+    print(f"  per page: wait for data {med(wait):.0f} cyc (p90 {np.percentile(wait, 90):.0f}), "
+          f"compute {med(comp):.0f} cyc (p90 {np.percentile(comp, 90):.0f})")
 
 
 def med(xs):
@@ -38,6 +65,9 @@ def main():
     seqs, heads = CASES[a.case]
     bk.attn_case(a.case, seqs, n_heads=heads)
     lib = native.load()
+    if a.case.startswith("dec"):
+        decode_report(lib, a.case)
+        return
     buf = np.zeros((CTAS, BLK, EV), dtype=np.uint32)
     fn = lib.gllm_debug_attn_trace_read
     fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
