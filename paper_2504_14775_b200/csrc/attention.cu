@@ -6,9 +6,10 @@
 //  * decode role (the item has one query token; `attn_decode_kernel<G, NW>`): NW = 4 or 8
 //    warps each walk pages w, w+NW, ... of the sequence through a 3-stage ring filled by 2-D
 //    TMA (one box per page and 64-dim half, 128B-swizzled so the ldmatrix fragment loads are
-//    conflict-free); the G query heads are one 16-row HMMA tile (mma.sync m16n8k16: this
-//    GEMV-shaped work is too small for a 128-row tcgen05 tile), online softmax on lane
-//    quads, warps merged through shared memory. HBM-bound by design. Pages before the last
+//    conflict-free); mma.sync m16n8k16 in transposed form (this GEMV-shaped work is too
+//    small for a 128-row tcgen05 tile): S^T = K.Q^T and O^T += V^T.P^T with 16 keys / dims as
+//    the MMA rows and the G <= 8 query heads as its 8 columns, online softmax across the
+//    warp's 8 lane groups, warps merged through shared memory. HBM-bound by design. Pages before the last
 //    one are fetched before griddepcontrol.wait (they predate this forward); a decode-only
 //    launch of few long sequences splits each sequence's pages over a cluster of up to 4
 //    CTAs whose partial (max, sum, O) rank 0 merges through distributed shared memory.
@@ -154,18 +155,26 @@ GLLM_DEVICE void ldsm_x4(uint32_t (&r)[4], const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
+// 8x8 b16 matrix in the mma fragment layout (thread: row lane / 4, columns 2 (lane % 4) + {0, 1})
+// -> its transpose in the same layout
+GLLM_DEVICE uint32_t movmatrix_trans(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
 GLLM_DEVICE void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
 
-// Decode role: one query token, the G query heads of kv head `kvh` padded to a
-// 16-row MMA tile. Each warp streams its pages (w, w+NW, ...) of [p_begin, p_end) through a
-// 3-stage TMA ring and per 16-key page issues 16 HMMA for S = Q.K^T and 16 for
-// O += P.V (P reused from the S accumulator registers), with the online softmax
-// on quads of lanes (one query head per quad). Warps merge through smem; with a KV split
-// (csize > 1) the ranks of the cluster then merge through rank 0's DecodeRed.
+// Decode role: one query token, the G query heads of kv head `kvh` as the 8 columns of
+// m16n8k16 MMAs. Each warp streams its pages (w, w+NW, ...) of [p_begin, p_end) through an
+// ST-stage TMA ring and per 16-key page issues 8 HMMA for S^T = K.Q^T and 8 for
+// O^T += V^T.P^T (P^T moved from the S^T accumulators into B fragments by movmatrix), with
+// the online softmax of each head across the lane groups holding its 16 keys. Warps merge
+// through smem; with a KV split (csize > 1) the ranks of the cluster then merge through rank 0's
+// DecodeRed.
 template <int G, int NW, int ST = DEC_STAGES>
 __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __restrict__ qkv, int tok, int kv_len,
                                             const int* __restrict__ table, const CUtensorMap* k_map,
@@ -179,8 +188,6 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   constexpr int HALF_BYTES = 16 * 128;  // one 64-dim box of a 16-slot page (8-slot pages use half)
   DecodeSmem<NW, ST>& sm = *reinterpret_cast<DecodeSmem<NW, ST>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qr = lane >> 2;          // fragment row = query head within the group
-  const int qc = (lane & 3) * 2;     // fragment column pair
   const int qkv_w = (n_heads + 2 * n_kv) * HD;
   const uint32_t page_bytes = (uint32_t)page_size * HD * 2;
   const int n_pages_all = (kv_len + page_size - 1) / page_size;
@@ -191,13 +198,17 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   if (lane == 0) {
     for (int s = 0; s < ST; ++s) mbar_init(&sm.full[warp][s], 1);
     fence_barrier_init();
+    if (warp == 0) {  // the tensor maps' descriptors, fetched once per CTA ahead of the first TMA
+      tma_prefetch_desc(k_map);
+      tma_prefetch_desc(v_map);
+    }
   }
   __syncwarp();
   // One page of one kv head = page_size rows x 128 dims; two 64-dim TMA boxes per tensor,
   // landing 128B-swizzled (row r, 16B chunk c at r*128 + ((c ^ r%8) << 4)) so the ldmatrix
   // fragment loads below are bank-conflict free.
-  auto issue = [&](int p, int s) {
-    const int row0 = (table[p] * n_kv + kvh) * page_size;
+  auto issue_page = [&](int page, int s) {
+    const int row0 = (page * n_kv + kvh) * page_size;
     mbar_arrive_expect_tx(&sm.full[warp][s], 2 * page_bytes);
     tma_load_2d(k_map, &sm.full[warp][s], sm.kv[warp][s][0], 0, row0);
     tma_load_2d(k_map, &sm.full[warp][s], sm.kv[warp][s][0] + HALF_BYTES, 64, row0);
@@ -210,36 +221,49 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
   // griddepcontrol.wait, overlapping the QKV GEMM. The last page holds this token's K/V, written
   // by that GEMM's epilogue (and may be newly appended to the table): it waits, as does Q.
   const int p_last = n_pages_all - 1;
-  if (lane == 0) {
-    for (int s = 0; s < ST; ++s) {
-      const int p = p_begin + warp + s * NW;
-      if (p < n_pages && p < p_last) issue(p, s);
-    }
+  // lane s reads the block-table entry of the warp's s-th page: one parallel round trip instead
+  // of ST dependent ones before the first TMA
+  int pre_page = 0;
+  if (lane < ST) {
+    const int p = p_begin + warp + lane * NW;
+    if (p < n_pages && p < p_last) pre_page = table[p];
+  }
+  for (int s = 0; s < ST; ++s) {
+    const int p = p_begin + warp + s * NW;
+    const int pg = __shfl_sync(0xffffffffu, pre_page, s);
+    if (lane == 0 && p < n_pages && p < p_last) issue_page(pg, s);
   }
   pdl_wait();
   if (lane == 0) {
     for (int s = 0; s < ST; ++s) {
       const int p = p_begin + warp + s * NW;
-      if (p < n_pages && p == p_last) issue(p, s);
+      if (p < n_pages && p == p_last) issue_page(table[p], s);
     }
   }
-  // Q as A fragments (rows >= G are zero), 8 k-steps of 16 dims.
-  uint32_t qa[8][4];
+  // Transposed form, so the MMA's M (16 rows) runs over keys and its N (8) over the G <= 8
+  // query heads instead of padding G heads to 16 rows: S^T = K . Q^T (A = a 16-key x 16-dim K
+  // block via ldmatrix, B = Q^T from registers) and O^T += V^T . P^T (A = V^T via
+  // ldmatrix.trans, B = P^T moved from the S^T accumulator layout by movmatrix.trans): 16
+  // m16n8k16 MMAs per 16-key page instead of 32. Thread (gid = lane / 4, tid = lane % 4) holds
+  // keys gid and gid + 8 of heads 2 tid and 2 tid + 1.
+  const int gid = lane >> 2, tid = lane & 3;
+  const int h0 = 2 * tid;
+  // Q^T as B fragments (heads >= G are zero), 8 k-steps of 16 dims: head gid, dims 2 tid (+8)
+  uint32_t qb[8][2];
   {
-    const bf16* qrow = qkv + (size_t)tok * qkv_w + (kvh * G + qr) * HD;
+    const bool live = gid < G;
+    const bf16* qrow = qkv + (size_t)tok * qkv_w + (kvh * G + (live ? gid : 0)) * HD;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const bool live = qr < G;
-      qa[kk][0] = live ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + qc) : 0u;
-      qa[kk][1] = 0u;
-      qa[kk][2] = live ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + qc) : 0u;
-      qa[kk][3] = 0u;
+      qb[kk][0] = live ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + h0) : 0u;
+      qb[kk][1] = live ? *reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + h0) : 0u;
     }
   }
-  float o[16][4];
+  float o[8][4];  // O^T: 16-dim tile mt; (dim 16 mt + gid, heads h0 / h0 + 1), (dim + 8, ...)
 #pragma unroll
-  for (int nb = 0; nb < 16; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
-  float m_run = -FLT_MAX, l_run = 0.f;   // row qr's state, replicated across its quad
+  for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+  float m_run[2] = {-FLT_MAX, -FLT_MAX}, l_run[2] = {0.f, 0.f};   // heads h0, h0 + 1
+  const int j = lane >> 3, r = lane & 7;  // ldmatrix: this lane addresses row r of matrix j
 
   int it = 0;
   for (int p = p_begin + warp; p < n_pages; p += NW, ++it) {
@@ -257,94 +281,95 @@ __device__ __forceinline__ void decode_role(uint8_t* smem_raw, const bf16* __res
             make_uint4(0, 0, 0, 0);
       __syncwarp();
     }
-    // ---- S = Q K^T : per 8-key n-block, 8 k-steps
-    float sc[2][4];
+    // ---- S^T = K . Q^T: 8 k-steps of 16 dims; matrix j = (keys 8 (j & 1).., dims 8 (j >> 1)..);
+    // even / odd k-steps in two accumulators (two dependent MMA chains of 4, not one of 8)
+    float sc[4] = {0.f, 0.f, 0.f, 0.f}, sc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) sc[nb][0] = sc[nb][1] = sc[nb][2] = sc[nb][3] = 0.f;
-#pragma unroll
-    for (int kk2 = 0; kk2 < 8; kk2 += 2) {
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        if (nb >= nblk) break;
-        // 4 matrices: (keys nb*8.., dims kk2*16 + {0,8}) and (.., dims (kk2+1)*16 + {0,8})
-        const int j = lane >> 3, r = lane & 7;
-        const int c = (kk2 & 3) * 2 + j;              // 16B chunk within the 64-dim half
-        uint32_t kb[4];
-        ldsm_x4(kb, kp + (kk2 >> 2) * HALF_BYTES + (nb * 8 + r) * 128 + ((c ^ r) << 4));
-        mma_16816_bf16(sc[nb], qa[kk2], kb[0], kb[1]);
-        mma_16816_bf16(sc[nb], qa[kk2 + 1], kb[2], kb[3]);
-      }
-    }
-    // ---- online softmax for row qr over this page's keys (4 per lane in its quad)
-    float mx = m_run;
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int key = nb * 8 + qc + e;
-        const bool valid = nb < nblk && key < keys_here;
-        const float x = sc[nb][e] * scale_log2;
-        sc[nb][e] = valid ? x : -FLT_MAX;
-        mx = fmaxf(mx, sc[nb][e]);
-      }
-    }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float corr = (m_run == -FLT_MAX) ? 0.f : exp2f(m_run - mx);
-    m_run = mx;
-    float psum = 0.f;
-    uint32_t pa[4];
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      const float p0 = sc[nb][0] == -FLT_MAX ? 0.f : exp2f(sc[nb][0] - mx);
-      const float p1 = sc[nb][1] == -FLT_MAX ? 0.f : exp2f(sc[nb][1] - mx);
-      psum += p0 + p1;
-      pa[nb * 2] = pack_bf16x2(p0, p1);  // a0a1 (keys 0-7) / a4a5 (keys 8-15) of row qr
-      pa[nb * 2 + 1] = 0u;               // rows 8-15 are padding
-    }
-    psum += __shfl_xor_sync(0xffffffffu, psum, 1);
-    psum += __shfl_xor_sync(0xffffffffu, psum, 2);
-    l_run = l_run * corr + psum;
-    if (__any_sync(0xffffffffu, corr != 1.f)) {
-#pragma unroll
-      for (int nb = 0; nb < 16; ++nb) {
-        o[nb][0] *= corr;
-        o[nb][1] *= corr;
-      }
-    }
-    // ---- O += P V : A = P (row qr; keys 0-7 in reg 0, 8-15 in reg 2), B = V via ldmatrix.trans
-    const uint32_t a_frag[4] = {pa[0], pa[1], nblk > 1 ? pa[2] : 0u, pa[3]};
-#pragma unroll
-    for (int nb = 0; nb < 16; nb += 2) {
-      const int j = lane >> 3, r = lane & 7;
+    for (int kk = 0; kk < 8; ++kk) {
       const int key = (j & 1) * 8 + r;
-      const int dblk = nb + (j >> 1);                 // 8-dim block 0..15
-      uint32_t vb[4];
-      ldsm_x4_t(vb, vp + (dblk >> 3) * HALF_BYTES + (key < page_size ? key : 0) * 128 + (((dblk & 7) ^ r) << 4));
-      if (nblk < 2) { vb[1] = 0u; vb[3] = 0u; }
-      mma_16816_bf16(o[nb], a_frag, vb[0], vb[1]);
-      mma_16816_bf16(o[nb + 1], a_frag, vb[2], vb[3]);
+      const int c = (kk & 3) * 2 + (j >> 1);          // 16B chunk within the 64-dim half
+      uint32_t ka[4];
+      ldsm_x4(ka, kp + (kk >> 2) * HALF_BYTES + (key < page_size ? key : 0) * 128 + ((c ^ r) << 4));
+      if (nblk < 2) { ka[1] = 0u; ka[3] = 0u; }      // 8-slot pages: keys 8-15 do not exist
+      mma_16816_bf16(kk & 1 ? sc2 : sc, ka, qb[kk][0], qb[kk][1]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sc[e] += sc2[e];
+    // ---- online softmax per head over this page's 16 keys (8 lane groups x 2 keys)
+    float x[2][2];   // [key gid / gid + 8][head h0 / h0 + 1]
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool valid = gid + 8 * k < keys_here;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) x[k][h] = valid ? sc[2 * k + h] * scale_log2 : -FLT_MAX;
+    }
+    float mx[2], corr[2], ps[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mx[h] = fmaxf(m_run[h], fmaxf(x[0][h], x[1][h]));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 4));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 8));
+      mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 16));
+      corr[h] = (m_run[h] == -FLT_MAX) ? 0.f : exp2f(m_run[h] - mx[h]);
+      m_run[h] = mx[h];
+    }
+    float pv[2][2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) pv[k][h] = x[k][h] == -FLT_MAX ? 0.f : exp2f(x[k][h] - mx[h]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      ps[h] = pv[0][h] + pv[1][h];
+      ps[h] += __shfl_xor_sync(0xffffffffu, ps[h], 4);
+      ps[h] += __shfl_xor_sync(0xffffffffu, ps[h], 8);
+      ps[h] += __shfl_xor_sync(0xffffffffu, ps[h], 16);
+      l_run[h] = l_run[h] * corr[h] + ps[h];
+    }
+    if (__any_sync(0xffffffffu, corr[0] != 1.f || corr[1] != 1.f)) {
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= corr[0];
+        o[mt][1] *= corr[1];
+        o[mt][2] *= corr[0];
+        o[mt][3] *= corr[1];
+      }
+    }
+    // P^T (keys x heads, accumulator layout) -> B fragments (k = keys, n = heads)
+    const uint32_t pb0 = movmatrix_trans(pack_bf16x2(pv[0][0], pv[0][1]));   // keys 0-7
+    const uint32_t pb1 = movmatrix_trans(pack_bf16x2(pv[1][0], pv[1][1]));   // keys 8-15
+    // ---- O^T += V^T . P^T: 8 tiles of 16 dims; matrix j = (dims 8 (j & 1).., keys 8 (j >> 1)..)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int key = (j >> 1) * 8 + r;
+      const int db = mt * 2 + (j & 1);                  // 8-dim block 0..15
+      uint32_t va[4];
+      ldsm_x4_t(va, vp + (db >> 3) * HALF_BYTES + (key < page_size ? key : 0) * 128 + (((db & 7) ^ r) << 4));
+      if (nblk < 2) { va[2] = 0u; va[3] = 0u; }
+      mma_16816_bf16(o[mt], va, pb0, pb1);
     }
     __syncwarp();
     const int pn = p + ST * NW;
     if (lane == 0 && pn < n_pages) {
       fence_proxy_async();
-      issue(pn, s);
+      issue_page(table[pn], s);
     }
     DEC_TRACE(it, 2);
   }
-  // ---- merge the 4 warps through smem (rows < G only); the ring is reused, so all
+  // ---- merge the NW warps through smem (heads < G only); the ring is reused, so all
   // warps must be done with their pages first
   __syncthreads();
-  if (qr < G) {
-    if ((lane & 3) == 0) {
-      sm.merge_m[warp][qr] = m_run;
-      sm.merge_l[warp][qr] = l_run;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h0 + h >= G) continue;
+    if (gid == 0) {
+      sm.merge_m[warp][h0 + h] = m_run[h];
+      sm.merge_l[warp][h0 + h] = l_run[h];
     }
 #pragma unroll
-    for (int nb = 0; nb < 16; ++nb) {
-      sm.merge_acc[warp][qr][nb * 8 + qc] = o[nb][0];
-      sm.merge_acc[warp][qr][nb * 8 + qc + 1] = o[nb][1];
+    for (int mt = 0; mt < 8; ++mt) {
+      sm.merge_acc[warp][h0 + h][mt * 16 + gid] = o[mt][h];
+      sm.merge_acc[warp][h0 + h][mt * 16 + 8 + gid] = o[mt][2 + h];
     }
   }
   __syncthreads();
