@@ -106,6 +106,36 @@ def gemm_case(M, N, K, bn=0, splits=0, swiglu=False, wscale=1.0):
                       "cublas_ms": round(ref, 4), "cublas_TFLOP/s": round(fl / ref / 1e9, 1)}))
 
 
+def qkv_rope_case(M, model="llama3-8b", ps=16):
+    """Fused QKV GEMM + RoPE + paged KV write (the stage's QKV launch) vs the plain GEMM of the same shape."""
+    from paper_2504_14775_b200.modelspec import MODELS, rope_table
+    spec = MODELS[model]
+    H, KV, d = spec.n_heads, spec.n_kv_heads, spec.d_model
+    Q = spec.qkv_width
+    A = torch.randn(M, d, device="cuda").bfloat16()
+    W = (torch.randn(Q, d, device="cuda") * 0.02).bfloat16()
+    bias = torch.randn(Q, device="cuda").bfloat16() if spec.qkv_bias else None
+    rope = torch.from_numpy(rope_table(spec, 8192)).cuda()
+    pos = torch.randint(0, 8000, (M,), dtype=torch.int32, device="cuda")
+    n_pages = (M + ps - 1) // ps + 64
+    slot = torch.randperm(n_pages * ps, device="cuda")[:M].to(torch.int32)
+    kc = torch.zeros(n_pages, KV, ps, 128, device="cuda").bfloat16()
+    vc = torch.zeros_like(kc)
+    out = torch.empty(M, Q, device="cuda").bfloat16()
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    st = native.stream_handle()
+    fused = lambda: native.call("gllm_gemm_qkv_rope_bf16", A.data_ptr(), d, W.data_ptr(), d,
+                                None if bias is None else bias.data_ptr(), out.data_ptr(), M, d, H, KV, pos.data_ptr(),
+                                slot.data_ptr(), rope.data_ptr(), kc.data_ptr(), vc.data_ptr(), ps, 0, 0,
+                                ws.data_ptr(), ws.numel(), st)
+    plain = lambda: native.call("gllm_gemm_bf16", A.data_ptr(), d, W.data_ptr(), d, out.data_ptr(), Q, M, Q, d,
+                                None, None, 0, 0, 0, ws.data_ptr(), ws.numel(), st)
+    tf, tp = timeit(fused), timeit(plain)
+    fl = 2 * M * Q * d
+    print(json.dumps({"kernel": "qkv_rope", "model": model, "M": M, "fused_ms": round(tf, 4), "plain_ms": round(tp, 4),
+                      "fused_TFLOP/s": round(fl / tf / 1e9, 1), "plain_TFLOP/s": round(fl / tp / 1e9, 1)}))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
@@ -113,7 +143,12 @@ if __name__ == "__main__":
     ap.add_argument("--wscale", type=float, default=1.0, help="weight std (0.02 = the stages' init)")
     ap.add_argument("--gemm", default="", help="M,N,K[,bn,splits] single GEMM case (bn/splits 0 = auto)")
     ap.add_argument("--swiglu", action="store_true")
+    ap.add_argument("--qkv-rope", default="", help="M[,model]: fused QKV + RoPE + KV write vs plain GEMM")
     a = ap.parse_args()
+    if a.qkv_rope:
+        v = a.qkv_rope.split(",")
+        qkv_rope_case(int(v[0]), *(v[1:2] or ["llama3-8b"]))
+        raise SystemExit(0)
     if a.gemm:
         v = [int(x) for x in a.gemm.split(",")] + [0, 0]
         gemm_case(v[0], v[1], v[2], bn=v[3], splits=v[4], swiglu=a.swiglu, wscale=a.wscale)
