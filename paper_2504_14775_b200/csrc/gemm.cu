@@ -645,6 +645,30 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       cg_pick = 2;
       whole_k = true;
     }
+    // 2 or 4 row tiles beyond that, K <= 16384: whole-K 2-CTA tiles of the width with the least
+    // wave-quantised work (waves x BN, ties to the wider tile) still beat split-K + reduce while
+    // the pairs keep half the SMs busy (M = 256, 10240 x 8192: BN 256 55.4 us vs split-K 3
+    // 68.6 us; M = 512: BN 128 80.0 vs 94.2 us; M = 512, 5120 x 13824: 83.9 vs 87.0 us; at
+    // K = 27648 split-K stays ahead).
+    if (!whole_k && m_tiles <= 4 && m_tiles % 2 == 0 && force_splits == 0 && cg_pref == 2 && K <= 16384) {
+      const long slots2 = num_sms / 2;
+      long best_w = 0;
+      int best_bn = 0;
+      for (int cand : {256, 128}) {
+        if (N % cand || cand < min_bn) continue;
+        const long units = (long)(m_tiles / 2) * (N / cand);
+        const long w = (units + slots2 - 1) / slots2 * cand;
+        if (best_bn == 0 || w < best_w) {
+          best_w = w;
+          best_bn = cand;
+        }
+      }
+      if (best_bn && (long)(m_tiles / 2) * (N / best_bn) * 2 * 2 >= num_sms) {
+        bn = best_bn;
+        cg_pick = 2;
+        whole_k = true;
+      }
+    }
     // One row tile (33-128 tokens past the decode kernel), short K: whole-K tiles of the
     // narrowest width the epilogue allows when they fill >= 1/4 of one wave (in a PDL chain at
     // M = 100: QKV 7168x5120 27.4 -> 21.7 us, 6144x4096 24.2 -> 18.2 us; K = 14336 stays split).
