@@ -645,12 +645,13 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       cg_pick = 2;
       whole_k = true;
     }
-    // 2 or 4 row tiles beyond that, K <= 16384: whole-K 2-CTA tiles of the width with the least
-    // wave-quantised work (waves x BN, ties to the wider tile) still beat split-K + reduce while
-    // the pairs keep half the SMs busy (M = 256, 10240 x 8192: BN 256 55.4 us vs split-K 3
-    // 68.6 us; M = 512: BN 128 80.0 vs 94.2 us; M = 512, 5120 x 13824: 83.9 vs 87.0 us; at
-    // K = 27648 split-K stays ahead).
-    if (!whole_k && m_tiles <= 4 && m_tiles % 2 == 0 && force_splits == 0 && cg_pref == 2 && K <= 16384) {
+    // 2 or 4 row tiles beyond that: whole-K 2-CTA tiles of the width with the least
+    // wave-quantised work (waves x BN, ties to the wider tile) beat split-K + reduce while the
+    // pairs keep half the SMs busy (M = 256, 10240 x 8192: BN 256 55.4 us vs split-K 3 68.6 us;
+    // M = 512: BN 128 80.0 vs 94.2 us; M = 512, 5120 x 13824: 83.9 vs 87.0 us), and for K > 16384
+    // when they fill >= 80% of the SMs in one wave (M = 256, 8192 x 28672: BN 128 104.4 vs
+    // 119.9 us; at 54% busy, 5120 x 27648, split-K stays ahead).
+    if (!whole_k && m_tiles <= 4 && m_tiles % 2 == 0 && force_splits == 0 && cg_pref == 2) {
       const long slots2 = num_sms / 2;
       long best_w = 0;
       int best_bn = 0;
@@ -663,7 +664,9 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
           best_bn = cand;
         }
       }
-      if (best_bn && (long)(m_tiles / 2) * (N / best_bn) * 2 * 2 >= num_sms) {
+      const long ctas = best_bn ? (long)(m_tiles / 2) * (N / best_bn) * 2 : 0;
+      const bool fits = K <= 16384 ? ctas * 2 >= num_sms : (ctas <= num_sms && ctas * 5 >= 4L * num_sms);
+      if (best_bn && fits) {
         bn = best_bn;
         cg_pick = 2;
         whole_k = true;
