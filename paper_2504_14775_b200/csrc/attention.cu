@@ -926,7 +926,7 @@ template <bool PREFILL, int G>
 static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, int n_work, const int* block_table,
                        int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache, int n_heads, int n_kv, int page_size,
                        float scale_log2, bf16* out, cudaStream_t st, const AttnSplit& sp = AttnSplit{},
-                       int dec_pages = 0) {
+                       int dec_pages = 0, int dec_mean_pages = 0) {
   constexpr size_t smem_pf = sizeof(PrefillSmem) + 1024;
   constexpr size_t smem4 = sizeof(DecodeSmem<4>) + 1024;
   constexpr size_t smem4s = sizeof(DecodeSmem<4, 2>) + 1024;   // 3 CTAs per SM
@@ -989,10 +989,14 @@ static int launch_attn(const bf16* qkv, const int* seq_info, const int* work, in
     // ring (the same pages in flight per SM) keep the items in one wave: e.g. 48-55 decodes with
     // 8 kv heads (384-440 items) against 296 two-per-SM slots.
     static const int three = [] {
-      const char* e = getenv("GLLM_DECODE_3CTA");  // A/B switch (default on)
+      const char* e = getenv("GLLM_DECODE_3CTA");  // A/B switch (default on; 2 = at every population)
       return e ? atoi(e) : 1;
     }();
-    const bool tri = !wide && three && items > 2L * sms && items <= 3L * sms;
+    // Beyond 1.5 waves too when the decodes are short (mean <= 64 pages, from the host metadata):
+    // C2's 800 x ~500-token decodes 270 -> 262 us (0.965 of HBM); at 2000-4000 tokens the 2-stage
+    // ring per warp loses 1-4%.
+    const bool tri = !wide && three && items > 2L * sms &&
+                     (items <= 3L * sms || three == 2 || (dec_mean_pages > 0 && dec_mean_pages <= 64));
     cudaError_t e = wide ? launch_kernel(attn_decode_kernel<G, 8>, grid, dim3(256), smem8, st, csize, km, vm, qkv,
                                          seq_info, work, block_table, mpr, n_heads, n_kv, page_size, scale_log2, out,
                                          csize)
@@ -1030,14 +1034,14 @@ template <int G>
 static int launch_attn_g(int n_prefill_work, const bf16* qkv, const int* seq_info, const int* work, int n_work,
                          const int* block_table, int mpr, int kv_pages, const bf16* k_cache, const bf16* v_cache,
                          int n_heads, int n_kv, int page_size, float scale_log2, bf16* out, cudaStream_t st,
-                         const AttnSplit& sp, int dec_pages) {
+                         const AttnSplit& sp, int dec_pages, int dec_mean_pages) {
   const int n_dec = n_work - n_prefill_work;
   if (n_prefill_work == 0)
     return launch_attn<false, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
-                                 n_kv, page_size, scale_log2, out, st, AttnSplit{}, dec_pages);
+                                 n_kv, page_size, scale_log2, out, st, AttnSplit{}, dec_pages, dec_mean_pages);
   if (n_dec == 0)
     return launch_attn<true, G>(qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads,
-                                n_kv, page_size, scale_log2, out, st, sp, dec_pages);
+                                n_kv, page_size, scale_log2, out, st, sp, dec_pages, dec_mean_pages);
   AttnStreams* ss = nullptr;
   if (int rc = attn_streams(&ss)) return rc;
   cudaEventRecord(ss->fork, st);
@@ -1046,7 +1050,7 @@ static int launch_attn_g(int n_prefill_work, const bf16* qkv, const int* seq_inf
                                 n_heads, n_kv, page_size, scale_log2, out, ss->side, sp);
   if (rc == 0)
     rc = launch_attn<false, G>(qkv, seq_info, work + 2 * n_prefill_work, n_dec, block_table, mpr, kv_pages, k_cache,
-                               v_cache, n_heads, n_kv, page_size, scale_log2, out, st);
+                               v_cache, n_heads, n_kv, page_size, scale_log2, out, st, AttnSplit{}, 0, dec_mean_pages);
   cudaEventRecord(ss->join, ss->side);
   cudaStreamWaitEvent(st, ss->join, 0);
   return rc;
@@ -1105,20 +1109,25 @@ int attention_paged(const bf16* qkv, const int* seq_info, const int* work, int n
       sp.part_ml = sp.part_o + (size_t)pf * n_split * n_kv * PTILES * PM * HD;
     }
   }
-  // decode-only launch: the longest decode's page count lets the decode kernel pick a KV split
-  int dec_pages = 0;
-  if (pf == 0 && host_seq_info && host_work)
-    for (int i = 0; i < n_work; ++i) {
+  // decode-only launch: the longest decode's page count lets the decode kernel pick a KV split;
+  // any launch: the decodes' mean page count picks its CTA shape
+  int dec_pages = 0, dec_mean_pages = 0;
+  if (host_seq_info && host_work && n_work > pf) {
+    long sum = 0;
+    for (int i = pf; i < n_work; ++i) {
       const int* si = host_seq_info + 5 * host_work[2 * i];
       const int pages = (si[1] + host_work[2 * i + 1] + 1 + page_size - 1) / page_size;
-      dec_pages = pages > dec_pages ? pages : dec_pages;
+      if (pf == 0) dec_pages = pages > dec_pages ? pages : dec_pages;
+      sum += pages;
     }
+    dec_mean_pages = (int)((sum + (n_work - pf) - 1) / (n_work - pf));
+  }
   switch (n_heads / n_kv) {
-    case 1: return launch_attn_g<1>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
-    case 2: return launch_attn_g<2>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
-    case 4: return launch_attn_g<4>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
-    case 5: return launch_attn_g<5>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
-    case 8: return launch_attn_g<8>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages);
+    case 1: return launch_attn_g<1>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages, dec_mean_pages);
+    case 2: return launch_attn_g<2>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages, dec_mean_pages);
+    case 4: return launch_attn_g<4>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages, dec_mean_pages);
+    case 5: return launch_attn_g<5>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages, dec_mean_pages);
+    case 8: return launch_attn_g<8>(pf, qkv, seq_info, work, n_work, block_table, mpr, kv_pages, k_cache, v_cache, n_heads, n_kv, page_size, scale_log2, out, st, sp, dec_pages, dec_mean_pages);
     default: return set_error(GLLM_ERR_INVALID, "unsupported GQA group %d", n_heads / n_kv);
   }
 }
