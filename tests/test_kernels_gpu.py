@@ -188,6 +188,20 @@ def test_gemm_qkv_rope_fused_matches_unfused(lib, M, name, splits):
     torch.cuda.synchronize()
     assert _rel(out[:, : H * 128], ref[:, : H * 128]) < 4e-3
     assert _rel(kf, kr) < 4e-3 and _rel(vf, vr) < 4e-3
+    # and against an fp32 torch reference of the whole fused op (GEMM + bias -> RoPE on q/k -> paged K/V)
+    x = A.float() @ W.float().T + (bias.float() if bias is not None else 0.0)
+    cs = rope[pos.long()]
+    c, s = cs[..., 0][:, None, :], cs[..., 1][:, None, :]
+
+    def rot(t):
+        return torch.cat([t[..., :64] * c - t[..., 64:] * s, t[..., 64:] * c + t[..., :64] * s], -1)
+    pg, off = (slot // ps).long(), (slot % ps).long()
+    q32 = rot(x[:, : H * 128].view(M, H, 128))
+    k32 = rot(x[:, H * 128:(H + KV) * 128].view(M, KV, 128))
+    v32 = x[:, (H + KV) * 128:].view(M, KV, 128)
+    errs = (_rel(out[:, : H * 128].view(M, H, 128), q32), _rel(kf[pg, :, off], k32), _rel(vf[pg, :, off], v32))
+    print(f"fused qkv+rope M={M} {name}: rel err vs fp32 q/k/v = {errs[0]:.2e} / {errs[1]:.2e} / {errs[2]:.2e}")
+    assert max(errs) < 8e-3, errs
     if splits == 1 and M >= 2000:   # same 256-wide tiles on both paths: bit-identical
         assert torch.equal(out[:, : H * 128], ref[:, : H * 128]) and torch.equal(kf, kr) and torch.equal(vf, vr)
 
