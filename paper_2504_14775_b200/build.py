@@ -20,7 +20,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgllm.so")
-SOURCES = ["gemm.cu", "gemm_skinny.cu", "kernels.cu", "attention.cu", "stage.cu"]
+SOURCES = ["gemm.cu", "gemm_swab.cu", "gemm_skinny.cu", "kernels.cu", "attention.cu", "stage.cu"]
 HEADERS = ["common.cuh", "gllm_internal.h"]
 
 

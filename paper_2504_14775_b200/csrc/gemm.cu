@@ -685,7 +685,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     if (m_tiles > 4 && force_splits == 0) {
       struct Cand { int cg, bn; double eff; };
       const Cand cands[] = {{2, 256, 0.85}, {2, 128, 0.75}, {1, 256, 0.75}, {1, 128, 0.55}, {1, 64, 0.37}};
-      double best = 1e30;
+      double best = 1e30;  // waves x BN / efficiency: per-SM work in units of 128 rows
       for (const Cand& c : cands) {
         if (N % c.bn || c.bn < min_bn || (c.cg == 2 && cg_pref != 2)) continue;
         const long units = (long)((M + BM * c.cg - 1) / (BM * c.cg)) * (N / c.bn);
@@ -696,6 +696,14 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
           bn = c.bn;
           cg_pick = c.cg;
         }
+      }
+      // swap-AB units (256 weights x a free token width; gemm_swab.cu) when they put less work on
+      // each SM: 128 x NT x waves against 128 x BN x waves (same modelled MMA efficiency)
+      if (!swiglu && !qkv && nm.ss_in == nullptr && cg_pref == 2) {
+        double w_swab = 0;
+        const int nt = gemm_swab_tile(M, N, K, &w_swab);
+        if (nt && w_swab / 0.85 < 0.98 * 128.0 * best)
+          return gemm_swab(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, nt, bias, residual, ldr, st, nm);
       }
     }
     while (bn > min_bn && N % bn) bn >>= 1;

@@ -24,7 +24,8 @@ def _rel(a, b):
 GEMM_SHAPES = [
     (1, 512, 256), (7, 256, 256), (64, 1536, 256), (128, 512, 4096), (130, 4096, 4096),
     (300, 6144, 4096), (1000, 4096, 14336), (33, 28672, 4096), (2048, 4096, 4096),
-    (2009, 6144, 4096),   # 192 2-CTA tiles over 74 clusters: 44-tile stream-K tail
+    (2009, 6144, 4096),
+    (2009, 4096, 14336),  # auto: swap-AB units of 512 weights x 224 tokens (gemm_swab.cu), bias + residual
 ]
 
 
@@ -109,7 +110,9 @@ def test_gemm_one_row_tile(lib, M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096),
-                                   (2009, 6144, 4096), (1500, 8192, 8192)])
+                                   (2009, 6144, 4096), (1500, 8192, 8192),
+                                   # swap-AB units: token widths 224 / 224 / 192 / 160, ragged last tiles
+                                   (2009, 4096, 4096), (1800, 4096, 14336), (1536, 4096, 4096), (1024, 5120, 5120)])
 def test_gemm_deterministic(lib, M, N, K):
     """Auto tiling (incl. split-K partial sums) is bit-stable across runs and agrees with whole-tile
     (force_splits=1) tiling to fp32 rounding."""

@@ -111,3 +111,13 @@ def test_long_prompts_chunked(cuda_ok, name, scheduler):
     _check(name, scheduler=scheduler, reqs=reqs, layers=4, pages=2048,
            throttle=ThrottleConfig(T=1, max_p=2048, min_p=32), token_budget=2048, oracle_device="cuda",
            max_tokens=4096)
+
+
+@pytest.mark.parametrize("name,budget", [("llama3-8b", 2009), ("llama3-8b", 1536), ("qwen2.5-14b", 1024)])
+def test_swap_ab_residual_gemms(cuda_ok, name, budget):
+    """Prefill micro-batches of 1-2k tokens (Sarathi budget = the batch size): the O / down projections
+    run the swap-AB units (gemm_swab.cu) whose epilogue also writes the fused-RMSNorm statistics that
+    the next QKV / gate-up GEMMs consume; logits vs the fp32 oracle."""
+    reqs = [RequestSpec(0, 0.0, 1500, 3), RequestSpec(1, 0.0, 700, 3), RequestSpec(2, 0.0, 400, 2)]
+    _check(name, scheduler="sarathi", reqs=reqs, layers=4, pages=1024, token_budget=budget, oracle_device="cuda",
+           max_tokens=4096)
