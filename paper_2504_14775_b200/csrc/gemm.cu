@@ -672,6 +672,17 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
         whole_k = true;
       }
     }
+    // 2 or 4 row tiles on whole-K 2-CTA tiles: swap-AB units instead when they put less work on
+    // each SM -- their free token width fills more clusters (M = 512, 5120 x 5120: 60 units of
+    // 256 weights x 192 tokens instead of 40 of 256 x 256)
+    if (whole_k && cg_pick == 2 && m_tiles <= 4 && !swiglu && !qkv && nm.ss_in == nullptr) {
+      const long units = (long)(m_tiles / 2) * (N / bn), slots2 = num_sms / 2;
+      const double cur = (double)((units + slots2 - 1) / slots2) * 128.0 * bn / (bn == 256 ? 0.85 : 0.75);
+      double w_swab = 0;
+      const int nt = gemm_swab_tile(M, N, K, &w_swab);
+      if (nt && w_swab / 0.85 < 0.98 * cur)
+        return gemm_swab(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, nt, bias, residual, ldr, st, nm);
+    }
     // One row tile (33-128 tokens past the decode kernel), short K: whole-K tiles of the
     // narrowest width the epilogue allows when they fill >= 1/4 of one wave (in a PDL chain at
     // M = 100: QKV 7168x5120 27.4 -> 21.7 us, 6144x4096 24.2 -> 18.2 us; K = 14336 stays split).

@@ -112,7 +112,8 @@ def test_gemm_one_row_tile(lib, M, N, K):
 @pytest.mark.parametrize("M,N,K", [(2048, 4096, 14336), (33, 28672, 4096), (1000, 4096, 4096), (3, 6144, 4096),
                                    (2009, 6144, 4096), (1500, 8192, 8192),
                                    # swap-AB units: token widths 224 / 224 / 192 / 160, ragged last tiles
-                                   (2009, 4096, 4096), (1800, 4096, 14336), (1536, 4096, 4096), (1024, 5120, 5120)])
+                                   (2009, 4096, 4096), (1800, 4096, 14336), (1536, 4096, 4096), (1024, 5120, 5120),
+                                   (512, 5120, 5120), (512, 5120, 13824), (480, 4096, 14336)])
 def test_gemm_deterministic(lib, M, N, K):
     """Auto tiling (incl. split-K partial sums) is bit-stable across runs and agrees with whole-tile
     (force_splits=1) tiling to fp32 rounding."""
