@@ -675,13 +675,14 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     // 2 or 4 row tiles on whole-K 2-CTA tiles: swap-AB units instead when they put less work on
     // each SM -- their free token width fills more clusters (M = 512, 5120 x 5120: 60 units of
     // 256 weights x 192 tokens instead of 40 of 256 x 256)
-    if (whole_k && cg_pick == 2 && m_tiles <= 4 && !swiglu && !qkv && nm.ss_in == nullptr) {
+    if (whole_k && cg_pick == 2 && m_tiles <= 4 && force_bn == 0 && !qkv) {
       const long units = (long)(m_tiles / 2) * (N / bn), slots2 = num_sms / 2;
       const double cur = (double)((units + slots2 - 1) / slots2) * 128.0 * bn / (bn == 256 ? 0.85 : 0.75);
       double w_swab = 0;
       const int nt = gemm_swab_tile(M, N, K, &w_swab);
       if (nt && w_swab / 0.85 < 0.98 * cur)
-        return gemm_swab(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, nt, bias, residual, ldr, st, nm);
+        return gemm_swab(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, nt, swiglu ? 2 : (qkv ? 3 : 0), bias, residual, ldr,
+                         qkv, st, nm);
     }
     // One row tile (33-128 tokens past the decode kernel), short K: whole-K tiles of the
     // narrowest width the epilogue allows when they fill >= 1/4 of one wave (in a PDL chain at
@@ -708,13 +709,15 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
           cg_pick = c.cg;
         }
       }
-      // swap-AB units (256 weights x a free token width; gemm_swab.cu) when they put less work on
-      // each SM: 128 x NT x waves against 128 x BN x waves (same modelled MMA efficiency)
-      if (!swiglu && !qkv && nm.ss_in == nullptr && cg_pref == 2) {
+      // swap-AB units (256 weights x a free token width; gemm_swab.cu, every fused epilogue) when
+      // they put less work on each SM: 128 x NT x waves against 128 x BN x waves
+      // (the QKV + RoPE epilogue stays on the 2-CTA tiles: measured slower through swab staging)
+      if (cg_pref == 2 && !qkv) {
         double w_swab = 0;
         const int nt = gemm_swab_tile(M, N, K, &w_swab);
         if (nt && w_swab / 0.85 < 0.98 * 128.0 * best)
-          return gemm_swab(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, nt, bias, residual, ldr, st, nm);
+          return gemm_swab(A, lda, a_rows_alloc, B, ldb, C, ldc, M, N, K, nt, swiglu ? 2 : (qkv ? 3 : 0), bias, residual, ldr,
+                         qkv, st, nm);
       }
     }
     while (bn > min_bn && N % bn) bn >>= 1;

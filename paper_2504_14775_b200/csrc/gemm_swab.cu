@@ -35,19 +35,22 @@ struct SwSmem {
   static constexpr int B_BYTES = (NT / 2) * SW_BK * 2;  // this CTA's half of the token box
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGING = NT * SW_WROWS * 2;     // bf16 [NT][128] epilogue staging
-  static constexpr int STAGES_FIT = (SW_SMEM_MAX - 1024 - 256 - STAGING) / STAGE;
+  static constexpr int STAGES_FIT = (SW_SMEM_MAX - 1024 - 256 - 1024 - STAGING) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr int RING = STAGES * STAGE;
-  static constexpr int TOTAL = 1024 + RING + STAGING + 256;
+  static constexpr int ROWSCALE = 256 * 4;             // fp32 row scale of the unit's tokens
+  static constexpr int TOTAL = 1024 + RING + STAGING + ROWSCALE + 256;
 };
 
 GLLM_DEVICE void sw_epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <int NT>
+enum : int { SW_STORE = 0, SW_SWIGLU = 2, SW_QKV_ROPE = 3 };  // gemm.cu's EPI_* numbering
+
+template <int NT, int MODE>
 __global__ void __launch_bounds__(SW_THREADS, 1)
 gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, int M,
                   int N, int K, bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
-                  const bf16* __restrict__ residual, int ldr, const RowNorm nm) {
+                  const bf16* __restrict__ residual, int ldr, const RowNorm nm, const QkvRopeArgs qa) {
   static_assert(NT % 32 == 0 && NT <= 256, "token tile: multiple of 32, at most 256");
   using L = SwSmem<NT>;
   constexpr int ST = L::STAGES;
@@ -55,7 +58,8 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   bf16* stg = reinterpret_cast<bf16*>(smem + L::RING);   // [NT][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RING + L::STAGING);
+  float* rs_s = reinterpret_cast<float*>(smem + L::RING + L::STAGING);  // [NT] row scales
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RING + L::STAGING + L::ROWSCALE);
   uint64_t* empty = full + ST;
   uint64_t* acc_full = empty + ST;   // [2] MMA -> epilogue
   uint64_t* acc_empty = acc_full + 2;  // [2] epilogue -> MMA
@@ -172,22 +176,34 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       const int acc = lt & 1;
       const int wrow = n0 + (int)rank * SW_WROWS;   // this CTA's first weight row / output column
       const float b_mine = bias != nullptr ? bf2f(bias[wrow + q * 32 + lane]) : 0.f;
+      if (nm.ss_in != nullptr) {  // fused RMSNorm: this unit's token row scales, once per unit
+        for (int j = t; j < NT; j += 128) rs_s[j] = m0 + j < M ? row_norm_scale(nm, m0 + j) : 1.f;
+        sw_epi_bar();
+      }
       mbar_wait(&acc_full[acc], (lt >> 1) & 1);
       tc_fence_after();
-      // TMEM (weight row = lane, token = column) -> bf16(acc + bias) staged as [token][weight]
+      // TMEM (weight row = lane, token = column) -> bf16(acc * row scale + bias) staged as
+      // [token][weight] (the roundings of gemm.cu's epilogues)
       const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256);
 #pragma unroll 1
       for (int j0 = 0; j0 < NT; j0 += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tb + (uint32_t)j0, r);
         tmem_ld_wait();
+        if (nm.ss_in != nullptr) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[(j0 + j) * SW_WROWS + q * 32 + lane] = f2bf(__uint_as_float(r[j]) + b_mine);
+          for (int j = 0; j < 32; ++j)
+            stg[(j0 + j) * SW_WROWS + q * 32 + lane] = f2bf(__uint_as_float(r[j]) * rs_s[j0 + j] + b_mine);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) stg[(j0 + j) * SW_WROWS + q * 32 + lane] = f2bf(__uint_as_float(r[j]) + b_mine);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(acc_empty_leader + (uint32_t)(acc * 8));  // TMEM buffer free
       sw_epi_bar();
+      if constexpr (MODE == SW_STORE) {
       const int col = wrow + 8 * c8;
       // 4 token rows per pass (rows j, j+8, j+16, j+24): their residual loads are in flight together
       constexpr int R = 4;
@@ -231,6 +247,68 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
           }
         }
       }
+      } else if constexpr (MODE == SW_SWIGLU) {
+        // the CTA's 128 weight rows are 64 gate rows then the 64 matching up rows (interleaved
+        // weight): lanes with c8 < 8 write act = bf16(silu(g)) * u for 8 output columns
+        const int ocol = (wrow >> 1) + 8 * (c8 & 7);
+#pragma unroll 2
+        for (int j = t >> 4; j < NT; j += 8) {
+          const int m = m0 + j;
+          if (c8 >= 8 || m >= M) continue;
+          const uint4 gv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * c8);
+          const uint4 uv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 64 + 8 * c8);
+          const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, uw[4] = {uv.x, uv.y, uv.z, uv.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 g = unpack_bf16x2(gw[e]), u = unpack_bf16x2(uw[e]);
+            const float a0 = bf2f(f2bf(silu_f(g.x))), a1 = bf2f(f2bf(silu_f(g.y)));
+            o[e] = pack_bf16x2(a0 * u.x, a1 * u.y);
+          }
+          *reinterpret_cast<uint4*>(C + (size_t)m * ldc + ocol) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      } else {
+        // QKV + RoPE + paged K/V write: the CTA's 128 weight rows are one whole head gh; lanes
+        // c8 < 8 hold dims d = 8 c8.. of the first half, c8 >= 8 the matching second half, and each
+        // reads its rotate-half partner from the staging tile
+        const int gh = wrow >> 7;
+        const int half = c8 >> 3, d0 = 8 * (c8 & 7);
+        const bool rotate = gh < qa.n_heads + qa.n_kv;
+#pragma unroll 2
+        for (int j = t >> 4; j < NT; j += 8) {
+          const int m = m0 + j;
+          if (m >= M) continue;
+          const uint4 xv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * c8);
+          uint4 out = xv;
+          if (rotate) {
+            const uint4 pv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * (c8 ^ 8));
+            const float2* cs = reinterpret_cast<const float2*>(qa.rope) + (size_t)qa.tok_pos[m] * 64 + d0;
+            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 x = unpack_bf16x2(xw[e]), pr = unpack_bf16x2(pw[e]);
+              const float2 c0 = cs[2 * e], c1 = cs[2 * e + 1];
+              // first half: p c - q s; second half: q c + p s (p = first-half value, q = second)
+              o[e] = half == 0 ? pack_bf16x2(x.x * c0.x - pr.x * c0.y, x.y * c1.x - pr.y * c1.y)
+                               : pack_bf16x2(x.x * c0.x + pr.x * c0.y, x.y * c1.x + pr.y * c1.y);
+            }
+            out = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+          bf16* dst;
+          if (gh < qa.n_heads) {
+            dst = C + (size_t)m * ldc + gh * 128;
+          } else {
+            const int slot = qa.tok_slot[m];
+            if (slot < 0) continue;  // metadata failed the bounds check in expand_tokens: no KV write
+            const int page = slot / qa.page_size, off = slot % qa.page_size;
+            const bool is_k = gh < qa.n_heads + qa.n_kv;
+            const int kvh = is_k ? gh - qa.n_heads : gh - qa.n_heads - qa.n_kv;
+            dst = (is_k ? qa.k_cache : qa.v_cache) + (((size_t)page * qa.n_kv + kvh) * qa.page_size + off) * 128;
+          }
+          *reinterpret_cast<uint4*>(dst + 8 * c8) = out;
+        }
+      }
       sw_epi_bar();  // staging is reused by the next unit
     }
   }
@@ -240,11 +318,11 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   if (warp == 1) tmem_dealloc_cg<2>(tmem_base, 512);
 }
 
-template <int NT>
+template <int NT, int MODE>
 int launch_swab(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, bf16* C, int ldc,
-                const bf16* bias, const bf16* res, int ldr, const RowNorm& nm, cudaStream_t st) {
+                const bf16* bias, const bf16* res, int ldr, const RowNorm& nm, const QkvRopeArgs& qa, cudaStream_t st) {
   constexpr int smem = SwSmem<NT>::TOTAL;
-  auto kern = gemm_swab_tcgen05<NT>;
+  auto kern = gemm_swab_tcgen05<NT, MODE>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -255,7 +333,7 @@ int launch_swab(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int 
   const long slots = device_sm_count() / 2;
   const int clusters = (int)(units < slots ? units : slots);
   cudaError_t e = launch_kernel(kern, dim3(2 * clusters), dim3(SW_THREADS), smem, st, 2, mw, mx, M, N, K, C, ldc, bias,
-                                res, ldr, nm);
+                                res, ldr, nm, qa);
   if (e != cudaSuccess) return set_cuda_error(e, "swab gemm launch");
   return check_launch("gemm_swab_tcgen05");
 }
@@ -287,19 +365,28 @@ int gemm_swab_tile(int M, int N, int K, double* work_per_sm) {
   return best_nt;
 }
 
+template <int NT>
+int launch_mode(int mode, const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, bf16* C, int ldc,
+                const bf16* bias, const bf16* res, int ldr, const RowNorm& nm, const QkvRopeArgs* qa, cudaStream_t st) {
+  if (mode == SW_SWIGLU) return launch_swab<NT, SW_SWIGLU>(mw, mx, M, N, K, C, ldc, nullptr, nullptr, 0, nm, QkvRopeArgs{}, st);
+  if (mode == SW_QKV_ROPE) return launch_swab<NT, SW_QKV_ROPE>(mw, mx, M, N, K, C, ldc, bias, nullptr, 0, nm, *qa, st);
+  return launch_swab<NT, SW_STORE>(mw, mx, M, N, K, C, ldc, bias, res, ldr, nm, QkvRopeArgs{}, st);
+}
+
 int gemm_swab(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,
-              int K, int nt, const bf16* bias, const bf16* residual, int ldr, cudaStream_t st, const RowNorm& nm) {
+              int K, int nt, int mode, const bf16* bias, const bf16* residual, int ldr, const QkvRopeArgs* qa,
+              cudaStream_t st, const RowNorm& nm) {
   if (ldc % 8 || (residual && ldr % 8)) return set_error(GLLM_ERR_INVALID, "gemm output pitch must be a multiple of 8");
-  if (nm.ss_in != nullptr) return set_error(GLLM_ERR_INVALID, "swab gemm: no input row scale");
+  if (mode == SW_QKV_ROPE && qa == nullptr) return set_error(GLLM_ERR_INVALID, "swab gemm: QKV mode needs its args");
   CUtensorMap mw, mx;
   if (int rc = make_tma_map_2d(&mw, W, N, K, ldw, SW_WROWS)) return rc;
   if (int rc = make_tma_map_2d(&mx, A, a_rows_alloc > M ? a_rows_alloc : M, K, lda, nt / 2)) return rc;
   switch (nt) {
-    case 128: return launch_swab<128>(mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, st);
-    case 160: return launch_swab<160>(mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, st);
-    case 192: return launch_swab<192>(mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, st);
-    case 224: return launch_swab<224>(mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, st);
-    case 256: return launch_swab<256>(mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, st);
+    case 128: return launch_mode<128>(mode, mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, qa, st);
+    case 160: return launch_mode<160>(mode, mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, qa, st);
+    case 192: return launch_mode<192>(mode, mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, qa, st);
+    case 224: return launch_mode<224>(mode, mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, qa, st);
+    case 256: return launch_mode<256>(mode, mw, mx, M, N, K, C, ldc, bias, residual, ldr, nm, qa, st);
     default: return set_error(GLLM_ERR_INVALID, "swab gemm: bad token tile %d", nt);
   }
 }

@@ -116,8 +116,10 @@ constexpr size_t GEMM_WS_HEAD_BYTES = 16384;  // skinny tile counters at the hea
 // gemm_swab.cu: swap-AB 2-CTA units of 256 weight rows x NT tokens for the store / residual
 // epilogue; gemm_swab_tile returns the token width NT (0 = not applicable) and its per-SM work.
 int gemm_swab_tile(int M, int N, int K, double* work_per_sm);
+// mode: 0 store (+bias/+residual, statistics out), 2 SwiGLU (interleaved gate/up), 3 QKV + RoPE + KV write
 int gemm_swab(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,
-              int K, int nt, const bf16* bias, const bf16* residual, int ldr, cudaStream_t st, const RowNorm& nm);
+              int K, int nt, int mode, const bf16* bias, const bf16* residual, int ldr, const QkvRopeArgs* qa,
+              cudaStream_t st, const RowNorm& nm);
 bool gemm_skinny_eligible(int M, int N, int K);
 size_t gemm_skinny_workspace_bytes(int M, int N, int K);
 int gemm_skinny(const bf16* A, int lda, int a_rows_alloc, const bf16* W, int ldw, bf16* C, int ldc, int M, int N,
