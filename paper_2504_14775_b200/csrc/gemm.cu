@@ -602,6 +602,22 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   return check_launch("gemm_bf16_tcgen05");
 }
 
+// The SwiGLU and QKV + RoPE epilogues of the swap-AB units are opt-in (GLLM_GEMM_SWAB_SWIGLU=1,
+// GLLM_GEMM_SWAB_QKV=1): faster in isolated microbenchmarks (gate-up 299 -> 292 us, fused QKV 86
+// -> 79 us at 2009 tokens) but 3-5% slower in the C2 step's ncu launch list, where their
+// epilogues also compute the fused-RMSNorm row scales (profiles/r2/launches_c2_swab_all.txt).
+static bool swab_mode_off(bool swiglu, bool qkv) {
+  static const bool sw = [] {
+    const char* e = getenv("GLLM_GEMM_SWAB_SWIGLU");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  static const bool qk = [] {
+    const char* e = getenv("GLLM_GEMM_SWAB_QKV");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  return (swiglu && !sw) || (qkv && !qk);
+}
+
 // swiglu != 0: B is the 64-row-interleaved [gate|up] weight (N = 2*d_ff) and C receives
 // act = silu(gate) * up as [M, N/2]; tiles must cover whole 128-row gate/up pairs (BN >= 128).
 static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, int ldc, int M, int N, int K,
@@ -675,7 +691,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
     // 2 or 4 row tiles on whole-K 2-CTA tiles: swap-AB units instead when they put less work on
     // each SM -- their free token width fills more clusters (M = 512, 5120 x 5120: 60 units of
     // 256 weights x 192 tokens instead of 40 of 256 x 256)
-    if (whole_k && cg_pick == 2 && m_tiles <= 4 && force_bn == 0 && !qkv) {
+    if (whole_k && cg_pick == 2 && m_tiles <= 4 && force_bn == 0 && !qkv && !swab_mode_off(swiglu, false)) {
       const long units = (long)(m_tiles / 2) * (N / bn), slots2 = num_sms / 2;
       const double cur = (double)((units + slots2 - 1) / slots2) * 128.0 * bn / (bn == 256 ? 0.85 : 0.75);
       double w_swab = 0;
@@ -711,8 +727,7 @@ static int gemm_impl(const bf16* A, int lda, const bf16* B, int ldb, bf16* C, in
       }
       // swap-AB units (256 weights x a free token width; gemm_swab.cu, every fused epilogue) when
       // they put less work on each SM: 128 x NT x waves against 128 x BN x waves
-      // (the QKV + RoPE epilogue stays on the 2-CTA tiles: measured slower through swab staging)
-      if (cg_pref == 2 && !qkv) {
+      if (cg_pref == 2 && !swab_mode_off(swiglu, qkv != nullptr)) {
         double w_swab = 0;
         const int nt = gemm_swab_tile(M, N, K, &w_swab);
         if (nt && w_swab / 0.85 < 0.98 * 128.0 * best)

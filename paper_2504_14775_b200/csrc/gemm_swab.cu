@@ -29,16 +29,17 @@ constexpr int SW_WROWS = 128;  // weight rows per CTA and unit (256 per cluster)
 constexpr int SW_THREADS = 192;
 constexpr int SW_SMEM_MAX = 227 * 1024;
 
-template <int NT>
+template <int NT, bool QKV = false>
 struct SwSmem {
   static constexpr int A_BYTES = SW_WROWS * SW_BK * 2;  // 16 KB weight box
   static constexpr int B_BYTES = (NT / 2) * SW_BK * 2;  // this CTA's half of the token box
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGING = NT * SW_WROWS * 2;     // bf16 [NT][128] epilogue staging
-  static constexpr int STAGES_FIT = (SW_SMEM_MAX - 1024 - 256 - 1024 - STAGING) / STAGE;
+  // fp32 row scales of the unit's tokens (+ their positions and KV slots for the QKV epilogue)
+  static constexpr int ROWSCALE = (QKV ? 3 : 1) * 256 * 4;
+  static constexpr int STAGES_FIT = (SW_SMEM_MAX - 1024 - 256 - ROWSCALE - STAGING) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
   static constexpr int RING = STAGES * STAGE;
-  static constexpr int ROWSCALE = 256 * 4;             // fp32 row scale of the unit's tokens
   static constexpr int TOTAL = 1024 + RING + STAGING + ROWSCALE + 256;
 };
 
@@ -52,13 +53,15 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
                   int N, int K, bf16* __restrict__ C, int ldc, const bf16* __restrict__ bias,
                   const bf16* __restrict__ residual, int ldr, const RowNorm nm, const QkvRopeArgs qa) {
   static_assert(NT % 32 == 0 && NT <= 256, "token tile: multiple of 32, at most 256");
-  using L = SwSmem<NT>;
+  using L = SwSmem<NT, MODE == SW_QKV_ROPE>;
   constexpr int ST = L::STAGES;
   static_assert(ST >= 3, "smem ring too shallow");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   bf16* stg = reinterpret_cast<bf16*>(smem + L::RING);   // [NT][128]
   float* rs_s = reinterpret_cast<float*>(smem + L::RING + L::STAGING);  // [NT] row scales
+  int* pos_s = reinterpret_cast<int*>(rs_s + 256);                       // [NT] (QKV) token positions
+  int* slot_s = pos_s + 256;                                             // [NT] (QKV) KV slots
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RING + L::STAGING + L::ROWSCALE);
   uint64_t* empty = full + ST;
   uint64_t* acc_full = empty + ST;   // [2] MMA -> epilogue
@@ -176,8 +179,17 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       const int acc = lt & 1;
       const int wrow = n0 + (int)rank * SW_WROWS;   // this CTA's first weight row / output column
       const float b_mine = bias != nullptr ? bf2f(bias[wrow + q * 32 + lane]) : 0.f;
-      if (nm.ss_in != nullptr) {  // fused RMSNorm: this unit's token row scales, once per unit
-        for (int j = t; j < NT; j += 128) rs_s[j] = m0 + j < M ? row_norm_scale(nm, m0 + j) : 1.f;
+      if (nm.ss_in != nullptr || MODE == SW_QKV_ROPE) {
+        // per-token values of this unit, read once (overlapping its MMAs): fused-RMSNorm row
+        // scales, and for the QKV epilogue the positions and paged KV slots
+        for (int j = t; j < NT; j += 128) {
+          const int m = m0 + j;
+          if (nm.ss_in != nullptr) rs_s[j] = m < M ? row_norm_scale(nm, m) : 1.f;
+          if constexpr (MODE == SW_QKV_ROPE) {
+            pos_s[j] = m < M ? qa.tok_pos[m] : 0;
+            slot_s[j] = m < M ? qa.tok_slot[m] : -1;
+          }
+        }
         sw_epi_bar();
       }
       mbar_wait(&acc_full[acc], (lt >> 1) & 1);
@@ -274,39 +286,52 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         const int gh = wrow >> 7;
         const int half = c8 >> 3, d0 = 8 * (c8 & 7);
         const bool rotate = gh < qa.n_heads + qa.n_kv;
-#pragma unroll 2
-        for (int j = t >> 4; j < NT; j += 8) {
-          const int m = m0 + j;
-          if (m >= M) continue;
-          const uint4 xv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * c8);
-          uint4 out = xv;
+        const bool is_q = gh < qa.n_heads, is_k = !is_q && rotate;
+        const int kvh = is_k ? gh - qa.n_heads : gh - qa.n_heads - qa.n_kv;
+        bf16* cache = is_k ? qa.k_cache : qa.v_cache;
+        constexpr int R = 4;  // token rows per pass: their (cos, sin) loads are in flight together
+#pragma unroll 1
+        for (int jb = t >> 4; jb < NT; jb += 8 * R) {
+          float4 cs[R][4];
           if (rotate) {
-            const uint4 pv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * (c8 ^ 8));
-            const float2* cs = reinterpret_cast<const float2*>(qa.rope) + (size_t)qa.tok_pos[m] * 64 + d0;
-            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
-            uint32_t o[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 x = unpack_bf16x2(xw[e]), pr = unpack_bf16x2(pw[e]);
-              const float2 c0 = cs[2 * e], c1 = cs[2 * e + 1];
-              // first half: p c - q s; second half: q c + p s (p = first-half value, q = second)
-              o[e] = half == 0 ? pack_bf16x2(x.x * c0.x - pr.x * c0.y, x.y * c1.x - pr.y * c1.y)
-                               : pack_bf16x2(x.x * c0.x + pr.x * c0.y, x.y * c1.x + pr.y * c1.y);
+            for (int r = 0; r < R; ++r) {
+              const float4* src = reinterpret_cast<const float4*>(qa.rope + ((size_t)pos_s[jb + 8 * r] * 64 + d0) * 2);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) cs[r][e] = src[e];   // (cos, sin) of dims d0 + 2e, d0 + 2e + 1
             }
-            out = make_uint4(o[0], o[1], o[2], o[3]);
           }
-          bf16* dst;
-          if (gh < qa.n_heads) {
-            dst = C + (size_t)m * ldc + gh * 128;
-          } else {
-            const int slot = qa.tok_slot[m];
-            if (slot < 0) continue;  // metadata failed the bounds check in expand_tokens: no KV write
-            const int page = slot / qa.page_size, off = slot % qa.page_size;
-            const bool is_k = gh < qa.n_heads + qa.n_kv;
-            const int kvh = is_k ? gh - qa.n_heads : gh - qa.n_heads - qa.n_kv;
-            dst = (is_k ? qa.k_cache : qa.v_cache) + (((size_t)page * qa.n_kv + kvh) * qa.page_size + off) * 128;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int j = jb + 8 * r, m = m0 + j;
+            if (m >= M) continue;
+            const uint4 xv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * c8);
+            uint4 out = xv;
+            if (rotate) {
+              const uint4 pv = *reinterpret_cast<const uint4*>(stg + j * SW_WROWS + 8 * (c8 ^ 8));
+              const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w}, pw[4] = {pv.x, pv.y, pv.z, pv.w};
+              uint32_t o[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 x = unpack_bf16x2(xw[e]), pr = unpack_bf16x2(pw[e]);
+                const float4 c = cs[r][e];  // (cos, sin) of dim d0 + 2e, then of d0 + 2e + 1
+                // first half: p c - q s; second half: q c + p s (p = first-half value, q = second)
+                o[e] = half == 0 ? pack_bf16x2(x.x * c.x - pr.x * c.y, x.y * c.z - pr.y * c.w)
+                                 : pack_bf16x2(x.x * c.x + pr.x * c.y, x.y * c.z + pr.y * c.w);
+              }
+              out = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            bf16* dst;
+            if (is_q) {
+              dst = C + (size_t)m * ldc + gh * 128;
+            } else {
+              const int slot = slot_s[j];
+              if (slot < 0) continue;  // metadata failed the bounds check in expand_tokens: no KV write
+              const int page = slot / qa.page_size, off = slot % qa.page_size;
+              dst = cache + (((size_t)page * qa.n_kv + kvh) * qa.page_size + off) * 128;
+            }
+            *reinterpret_cast<uint4*>(dst + 8 * c8) = out;
           }
-          *reinterpret_cast<uint4*>(dst + 8 * c8) = out;
         }
       }
       sw_epi_bar();  // staging is reused by the next unit
@@ -321,7 +346,7 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
 template <int NT, int MODE>
 int launch_swab(const CUtensorMap& mw, const CUtensorMap& mx, int M, int N, int K, bf16* C, int ldc,
                 const bf16* bias, const bf16* res, int ldr, const RowNorm& nm, const QkvRopeArgs& qa, cudaStream_t st) {
-  constexpr int smem = SwSmem<NT>::TOTAL;
+  constexpr int smem = SwSmem<NT, MODE == SW_QKV_ROPE>::TOTAL;
   auto kern = gemm_swab_tcgen05<NT, MODE>;
   static bool attr_done = false;
   if (!attr_done) {

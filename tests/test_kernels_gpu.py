@@ -135,7 +135,7 @@ def test_gemm_deterministic(lib, M, N, K):
 
 
 @pytest.mark.parametrize("M,d_ff,K", [(1, 768, 256), (37, 14336, 4096), (300, 768, 256), (2048, 14336, 4096),
-                                      (2009, 14336, 4096)])   # auto: swap-AB units with the SwiGLU epilogue
+                                      (2009, 14336, 4096)])   # swap-AB SwiGLU epilogue when GLLM_GEMM_SWAB_SWIGLU=1
 def test_gemm_swiglu_fused(lib, M, d_ff, K):
     from paper_2504_14775_b200.modelspec import interleave_gate_up
     g = torch.Generator(device="cuda").manual_seed(M + d_ff)
@@ -158,7 +158,7 @@ def test_gemm_swiglu_fused(lib, M, d_ff, K):
 
 @pytest.mark.parametrize("M,name,splits", [(5, "llama3-8b", 0), (300, "llama3-8b", 0), (2009, "llama3-8b", 1),
                                            (77, "qwen2.5-14b", 1), (64, "qwen2.5-14b", 0), (130, "tiny", 1),
-                                           # auto: swap-AB units with the RoPE + KV-write epilogue (+ bias)
+                                           # swap-AB RoPE + KV-write epilogue (+ bias) when GLLM_GEMM_SWAB_QKV=1
                                            (2009, "llama3-8b", 0), (1024, "qwen2.5-14b", 0), (1500, "llama3.1-70b", 0)])
 def test_gemm_qkv_rope_fused_matches_unfused(lib, M, name, splits):
     """Fused QKV+RoPE+KV-write epilogue == GEMM(+bias) -> rope_kv_write (bit-identical when both use the same
