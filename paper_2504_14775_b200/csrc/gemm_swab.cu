@@ -8,8 +8,8 @@
 // ~2k tokens are 144 units of 256 weights x 224 tokens over 74 clusters (two per cluster:
 // 114,688 outputs on each) instead of 128 units of 256 x 256 (131,072 on the busiest) -- the tile
 // shape cuBLAS's nvjet kernels pick for these shapes (profiles/r2/cublas_kernel_names.txt).
-// Persistent like gemm.cu: a cluster of two CTAs walks units u = cluster, +#clusters, ... (token
-// tiles fastest); per 64-wide K-block each CTA TMA-loads its 128 weight rows and half of the NT
+// Persistent like gemm.cu: a cluster of two CTAs walks its units (one token tile, every #clusters-
+// per-tile-th weight tile; see the unit walk); per 64-wide K-block each CTA TMA-loads its 128 weight rows and half of the NT
 // token rows, the leader issues one M=256, N=NT cta_group::2 MMA per K-step into one of two TMEM
 // accumulators (columns 0 / 256), so the epilogue of unit i overlaps the MMAs of unit i+1.
 //
@@ -96,9 +96,29 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  auto coords = [&](int u, int& m0, int& n0) {
-    m0 = (u % m_tiles) * NT;  // token tiles fastest: concurrent units share weight boxes in L2
-    n0 = (u / m_tiles) * (2 * SW_WROWS);
+  // Unit walk. With at least one cluster per token tile, cluster c keeps token tile c % m_tiles for
+  // its whole run and steps over the weight tiles (c / m_tiles) + k x (clusters of that token
+  // tile): its per-token values (fused-norm row scales, positions, slots) are read once, and the
+  // clusters at step k of all token tiles share the same few weight tiles in L2. Otherwise (fewer
+  // units than clusters: one unit each, or when the token tiles' cluster counts do not divide the
+  // weight tiles evenly enough) units are dealt token-tile-fastest.
+  const int n_wt = N / (2 * SW_WROWS);
+  // (only when it costs no extra wave: the token tile with the fewest clusters sets the length)
+  const bool tt_major = ustride >= m_tiles &&
+                        (n_wt + ustride / m_tiles - 1) / (ustride / m_tiles) <= (units + ustride - 1) / ustride;
+  const int my_tt = unit0 % m_tiles, my_r = unit0 / m_tiles;
+  const int my_cpt = tt_major ? (ustride - 1 - my_tt) / m_tiles + 1 : 1;
+  const int my_units = tt_major ? (my_r < n_wt ? (n_wt - my_r + my_cpt - 1) / my_cpt : 0)
+                                : (unit0 < units ? (units - unit0 + ustride - 1) / ustride : 0);
+  auto coords = [&](int k, int& m0, int& n0) {
+    if (tt_major) {
+      m0 = my_tt * NT;
+      n0 = (my_r + k * my_cpt) * (2 * SW_WROWS);
+    } else {
+      const int u = unit0 + k * ustride;
+      m0 = (u % m_tiles) * NT;
+      n0 = (u / m_tiles) * (2 * SW_WROWS);
+    }
   };
 
   if (warp == 0) {
@@ -109,9 +129,9 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
         if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * L::STAGE);
       };
       int pre = 0;
-      if (unit0 < units) {  // the first unit's weights do not depend on the predecessor kernel
+      if (my_units > 0) {  // the first unit's weights do not depend on the predecessor kernel
         int m0, n0;
-        coords(unit0, m0, n0);
+        coords(0, m0, n0);
         pre = min(nkb, ST);
         for (int i = 0; i < pre; ++i) {
           expect(i);
@@ -121,9 +141,9 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
       }
       pdl_wait();  // the activations are the predecessor's output
       int it = 0;
-      for (int u = unit0; u < units; u += ustride) {
+      for (int k = 0; k < my_units; ++k) {
         int m0, n0;
-        coords(u, m0, n0);
+        coords(k, m0, n0);
         for (int i = 0; i < nkb; ++i, ++it) {
           const int s = it % ST;
           const uint32_t ph = (it / ST) & 1;
@@ -142,7 +162,7 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     if (rank == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(256, NT);
       int it = 0, lt = 0;
-      for (int u = unit0; u < units; u += ustride, ++lt) {
+      for (int k = 0; k < my_units; ++k, ++lt) {
         const int acc = lt & 1;
         mbar_wait(&acc_empty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -173,13 +193,13 @@ gemm_swab_tcgen05(const __grid_constant__ CUtensorMap map_w, const __grid_consta
     const int c8 = t & 15;                // this thread's 8 output columns of a token row
     const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
     int lt = 0;
-    for (int u = unit0; u < units; u += ustride, ++lt) {
+    for (int k = 0; k < my_units; ++k, ++lt) {
       int m0, n0;
-      coords(u, m0, n0);
+      coords(k, m0, n0);
       const int acc = lt & 1;
       const int wrow = n0 + (int)rank * SW_WROWS;   // this CTA's first weight row / output column
       const float b_mine = bias != nullptr ? bf2f(bias[wrow + q * 32 + lane]) : 0.f;
-      if (nm.ss_in != nullptr || MODE == SW_QKV_ROPE) {
+      if ((nm.ss_in != nullptr || MODE == SW_QKV_ROPE) && (k == 0 || !tt_major)) {
         // per-token values of this unit, read once (overlapping its MMAs): fused-RMSNorm row
         // scales, and for the QKV epilogue the positions and paged KV slots
         for (int j = t; j < NT; j += 128) {
